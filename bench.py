@@ -1,0 +1,434 @@
+"""Benchmark: grid-point x RK-stage updates/s per variant (BL/RA/SN/SS), fp64.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--n 64]
+                    [--variants BL,RA,SN,SS] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): Taylor-Green vortex 64^3, fp64,
+dt=3.385e-3, RK3 steps of each variant on one GPU.  A "step" is one full
+RK3 iteration (3 stages); the unit of work is one interior grid point
+advanced through one RK stage, so value = N^3 * 3 * K / seconds.
+
+Timing: W untimed warm-up steps, then K steps, each timed with CUDA events
+on the launching stream (the step is one captured CUDA graph); between
+timed steps L2 is flushed by writing a 256 MiB buffer (outside the events).
+Multi-GPU (torchrun): z-slab decomposition with NCCL halo exchange; the
+per-rank time is reduced with MAX; --scaling weak (default: each rank owns
+n planes, the grid is refined along axis 0) or strong (the n^3 grid split).
+
+--impl reference times the reference algorithm's CPU restatement (the C +
+OpenMP oracle, pinned bitwise to the reference) on the host cores; the
+reference package itself is pure Python/numba and does not exist on the GPU
+box.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("grid-pt·RK-stage updates/s per variant (BL/RA/SN/SS), fp64; "
+          "% of roofline")
+UNIT = "grid-pt*RK-stage/s"
+DT = {64: 3.385e-3, 128: 1.69e-3, 256: 8.5e-4, 512: 4.2e-4, 32: 2e-3}
+
+# Algorithmic per-point costs of one fused stage kernel:
+#   flops F_v = residual source flops + 10 (update) + 13 (primitives)
+#   bytes: model M for the fused stage = read 10 state fields + 5 saved
+#   (stage 0: saved == input) + write 10, plus each FETCH array written and
+#   read once by the fills/residual.
+RESIDUAL_FLOPS = {"BL": 223, "RA": 1318, "RS": 838, "SN": 895, "SS": 730}
+STAGE_FLOPS = {v: f + 23 for v, f in RESIDUAL_FLOPS.items()}
+N_WORK = {"BL": 60, "RA": 0, "RS": 9, "SN": 0, "SS": 9}
+
+
+def stage_bytes(v: str) -> float:
+    """Compulsory HBM bytes per point of one fused stage (avg over the 3
+    stages: stage 0 reads its saved fields as the input)."""
+    state = (10 + 5 * 2.0 / 3.0 + 10) * 8.0
+    return state + 2 * 8.0 * N_WORK[v]
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:6])
+                          if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ setup
+def init_dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def cpu_cores() -> int:
+    return len(os.sched_getaffinity(0))
+
+
+def run_cpu_oracle(n: int, steps: int, warmup: int = 1):
+    """The C + OpenMP restatement of the reference path (oracle/), timed on
+    the host cores: pt-stage/s."""
+    from oracle import c_oracle, numpy_oracle as npo
+    c = npo.Consts()
+    F = npo.taylor_green(n, c)
+    c_oracle.run(F, c, DT.get(n, 3.385e-3), warmup)
+    t0 = time.perf_counter()
+    c_oracle.run(F, c, DT.get(n, 3.385e-3), steps)
+    dt = time.perf_counter() - t0
+    return n ** 3 * 3 * steps / dt, dt
+
+
+# ------------------------------------------------------------------ ours
+def bench_variant(fd, variant, grid, steps, warmup, flush_buf, lib):
+    import torch
+    from paper_1610_09146_b200 import _lib
+    from paper_1610_09146_b200.timeloop import IterationState, _fused_iteration
+    c = fd.PhysicalConstants()
+    state = fd.taylor_green_init(grid, c)
+    ev = fd.ResidualEvaluator(grid, c, variant)
+    scheme = fd.RKScheme(dt=DT.get(grid.npoints[1], 3.385e-3))
+    it = IterationState(state, saved=False)
+    multi = grid.slab is not None and grid.slab.nranks > 1
+    for _ in range(warmup):
+        _fused_iteration(it, scheme, ev)
+    torch.cuda.synchronize()
+
+    graph = None
+    if not multi:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            _fused_iteration(it, scheme, ev)      # warm the capture stream
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            _fused_iteration(it, scheme, ev)
+        torch.cuda.synchronize()
+
+    def step():
+        if graph is not None:
+            graph.replay()
+        else:
+            _fused_iteration(it, scheme, ev)
+
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    n_launch0 = lib.fdns_launch_count()
+    launches_per_step = None
+    if graph is not None:
+        # graph replays do not pass through the ABI counter: count one
+        # eager step's launches instead
+        c0 = lib.fdns_launch_count()
+        _fused_iteration(it, scheme, ev)
+        launches_per_step = lib.fdns_launch_count() - c0
+    if multi:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    n_launch0 = lib.fdns_launch_count()
+    for k in range(steps):
+        _lib.check(lib.fdns_l2_flush(_lib.ptr(flush_buf), flush_buf.numel(),
+                                     _lib.stream_handle()), "flush")
+        evs[k][0].record(stream)
+        step()
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    if multi:
+        dist.barrier()
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    launches = (launches_per_step * steps if launches_per_step is not None
+                else lib.fdns_launch_count() - n_launch0)
+
+    # dominant kernel: the fused stage (residual+update+prims), timed alone
+    X = state.bundle
+    Y, Z = ev.workspace()
+    kev = [(torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(6)]
+    for a, b in kev:
+        _lib.check(lib.fdns_l2_flush(_lib.ptr(flush_buf), flush_buf.numel(),
+                                     _lib.stream_handle()), "flush")
+        a.record(stream)
+        ev.stage(Y, X, Z, 1e-30)   # same work as a real stage
+        b.record(stream)
+    torch.cuda.synchronize()
+    stage_ms = float(np.median([a.elapsed_time(b) for a, b in kev]))
+    del graph
+    return total_ms, launches, stage_ms
+
+
+def fp64_peak(lib):
+    """In-run FP64 issue-rate probe (DADD only, 1 flop per instruction)."""
+    import torch
+    from paper_1610_09146_b200 import _lib
+    import ctypes
+    scratch = torch.zeros(1, dtype=torch.float64, device="cuda")
+    cnt = ctypes.c_double(0)
+    iters = 20000
+    for _ in range(2):
+        _lib.check(lib.fdns_fp64_probe(_lib.ptr(scratch), iters,
+                                       ctypes.byref(cnt), _lib.stream_handle()))
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    reps = 5
+    for _ in range(reps):
+        _lib.check(lib.fdns_fp64_probe(_lib.ptr(scratch), iters,
+                                       ctypes.byref(cnt), _lib.stream_handle()))
+    b.record()
+    torch.cuda.synchronize()
+    sec = a.elapsed_time(b) / 1e3
+    return cnt.value * reps / sec / 1e12   # T FP64 instr/s == TFLOP/s (DADD)
+
+
+def bench_e2e(fd, variant, grid, steps):
+    """Same metric through the public API with host buffers: per step the
+    five conservative fields are copied H2D from pinned memory, one
+    `advance_iteration` runs, and the fields are copied back D2H."""
+    import torch
+    c = fd.PhysicalConstants()
+    state = fd.taylor_green_init(grid, c)
+    ev = fd.ResidualEvaluator(grid, c, variant)
+    scheme = fd.RKScheme(dt=DT.get(grid.npoints[1], 3.385e-3))
+    it = fd.IterationState(state)
+    host = torch.empty((5,) + grid.shape, dtype=torch.float64).pin_memory()
+    host.copy_(state.bundle[:5].cpu())
+    stream = torch.cuda.current_stream()
+    fd.advance_iteration(it, scheme, ev)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        state.bundle[:5].copy_(host, non_blocking=True)
+        fd.advance_iteration(it, scheme, ev)
+        host.copy_(state.bundle[:5], non_blocking=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    sec = a.elapsed_time(b) / 1e3
+    npts = float(np.prod(grid.npoints))
+    nbytes = host.numel() * 8
+    return {"value": npts * 3 * steps / sec, "unit": UNIT,
+            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+            "variant": variant}
+
+
+def main_ours(args):
+    import torch
+    rank, world, local = init_dist()
+    torch.cuda.set_device(local)
+    import paper_1610_09146_b200 as fd
+    from paper_1610_09146_b200 import _lib
+    lib = _lib.load()
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    n = args.n
+    slab = None
+    if world > 1:
+        n0 = n * world if args.scaling == "weak" else n
+        slab = fd.Slab.from_process_group(n0)
+        grid = fd.make_grid((n0, n, n), (2 * np.pi,) * 3, slab=slab)
+    else:
+        grid = fd.make_grid((n, n, n), (2 * np.pi,) * 3)
+    npts_total = float(np.prod(grid.npoints))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    fp64_tf = fp64_peak(lib)
+    results = {}
+    with ClockSampler(local) as clocks:
+        for v in args.variants:
+            total_ms, launches, stage_ms = bench_variant(
+                fd, v, grid, args.steps, args.warmup, flush, lib)
+            if world > 1:
+                import torch.distributed as dist
+                t = torch.tensor([total_ms, stage_ms], device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                total_ms, stage_ms = t.tolist()
+            local_pts = float(np.prod(grid.local_npoints))
+            val = npts_total * 3 * args.steps / (total_ms / 1e3)
+            flops = STAGE_FLOPS[v] * local_pts / (stage_ms / 1e3) / 1e12
+            gbs = stage_bytes(v) * local_pts / (stage_ms / 1e3) / 1e9
+            t_fp64 = STAGE_FLOPS[v] / (fp64_tf * 1e12)
+            t_hbm = stage_bytes(v) / (hbm_peak * 1e9)
+            bound = "fp64" if t_fp64 >= t_hbm else "hbm"
+            results[v] = {
+                "value": val, "ms_per_step": total_ms / args.steps,
+                "gpu_launches": launches,
+                "stage_kernel_ms": stage_ms,
+                "stage_kernel_flops_per_pt": STAGE_FLOPS[v],
+                "stage_kernel_bytes_per_pt": stage_bytes(v),
+                "achieved_tflops": flops, "achieved_gbs": gbs,
+                "bound": bound,
+                "roofline_pt_stage_per_s": 1.0 / max(t_fp64, t_hbm),
+                "frac_of_roofline": (local_pts / (stage_ms / 1e3))
+                * max(t_fp64, t_hbm),
+            }
+    if rank != 0:
+        return
+    head = max(results, key=lambda v: results[v]["value"])
+    r = results[head]
+    if r["bound"] == "fp64":
+        roof = {"bound": "fp64", "achieved": r["achieved_tflops"],
+                "peak": fp64_tf, "unit": "TFLOP/s",
+                "peak_source": "measured in-run (DADD issue probe, no-FMA)"}
+    else:
+        roof = {"bound": "hbm", "achieved": r["achieved_gbs"],
+                "peak": hbm_peak, "unit": "GB/s",
+                "peak_source": f"{hbm_src} (MEASURED_PEAKS.json hbm_gbs)"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = f"fused stage ({head}): residual+RK update+primitives"
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cpu_steps = max(1, args.cpu_steps)
+        v, sec = run_cpu_oracle(n, cpu_steps)
+        cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+               "sample": f"C+OpenMP oracle (SN route), TGV {n}^3, "
+                         f"{cpu_steps} RK3 steps after 1 warm-up, {sec:.1f} s"}
+    e2e = bench_e2e(fd, head, grid, max(3, min(args.steps, 20))) \
+        if world == 1 else None
+
+    line = {
+        "metric": METRIC, "value": r["value"], "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+        "scaling": args.scaling if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: analytic Taylor-Green vortex initial state "
+                "(BASELINE.json configs[1])",
+        "config": {"workload": f"TGV {n}^3 fp64, dt={DT.get(n)}, RK3 steps, "
+                               "variants " + "/".join(args.variants),
+                   "grid": list(grid.npoints), "headline_variant": head,
+                   "parallelism": f"z-slab x{world}",
+                   "l2": "flushed between timed steps (256 MiB write)"},
+        "variants": {v: {k: x for k, x in d.items()} for v, d in results.items()},
+        "roofline": roof,
+        "fp64_peak_tflops_measured": fp64_tf,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": r["gpu_launches"],
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line))
+
+
+def main_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    n = args.n
+    steps = max(1, min(args.steps, args.cpu_steps))
+    for _ in range(args.warmup and 1):
+        pass
+    val, sec = run_cpu_oracle(n, steps, warmup=1)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
+        "n_gpus": world, "steps": steps, "warmup": 1,
+        "ms_per_step": sec / steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: analytic Taylor-Green vortex initial state",
+        "config": {"workload": f"TGV {n}^3 fp64, dt={DT.get(n)}, RK3 steps",
+                   "grid": [n, n, n]},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cpu_cores(),
+                         "kind": "port",
+                         "sample": f"C+OpenMP restatement of the reference "
+                                   f"(SN route), TGV {n}^3, {steps} steps"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--n", type=int, default=64)
+    ap.add_argument("--variants", default="BL,RA,SN,SS")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--cpu-steps", type=int, default=20)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.variants = [v.strip().upper() for v in args.variants.split(",")]
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        main_reference(args)
+    else:
+        main_ours(args)
+
+
+if __name__ == "__main__":
+    main()

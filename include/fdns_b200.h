@@ -1,0 +1,112 @@
+/*
+ * fdns_b200.h -- C ABI of the B200-native fdns hot path.
+ *
+ * Plain C: raw device pointers, sizes, a cudaStream_t passed as void*, and an
+ * int status (0 = ok; otherwise fdns_last_error() describes the failure).
+ * No torch types cross this boundary; the Python host layer
+ * (paper_1610_09146_b200/_lib.py) binds it with ctypes and torch only owns
+ * the buffers.
+ *
+ * Storage: every field is a float64 array C-ordered (n0+2h, n1+2h, n2+2h),
+ * axis 2 contiguous -- byte-identical to the reference's padded numpy arrays
+ * (pkg/src/fdns/mesh.py:3-6).  A "bundle" is `nf` such fields back to back at
+ * a field stride of (n0+2h)(n1+2h)(n2+2h) elements; the state bundle holds
+ * rho, rhou0, rhou1, rhou2, rhoE, u0, u1, u2, p, T in the reference's kernel
+ * argument order (pkg/src/fdns/physics.py:115-119).  For a z-slab rank, n0 is
+ * the number of local planes along axis 0.
+ *
+ * Reference interfaces each entry point replaces are cited per function
+ * (paths relative to /root/reference/pkg/src/fdns/).
+ */
+#ifndef FDNS_B200_H
+#define FDNS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Variant ids: the reference's PLAN_NAMES (plan.py:33). */
+enum fdns_variant { FDNS_BL = 0, FDNS_RA = 1, FDNS_RS = 2, FDNS_SN = 3, FDNS_SS = 4 };
+
+/* Problem description shared by every call. */
+typedef struct fdns_problem {
+  int32_t n[3];      /* interior points per axis (n[0] = local planes) */
+  int32_t h;         /* halo width (>= 2; mesh.py:17,82) */
+  double w[15];      /* (fw1, fw2, s0, s1, s2) per axis (plan.py:339-344) */
+  double kc[5];      /* inv_Re, c13, c43, c23, heat_coeff (physics.py:78-81) */
+  double gm1, gM2;   /* gamma-1, gamma*M*M (physics.py:53-58) */
+} fdns_problem;
+
+/* Text of the last failure on this thread ("" if none). */
+const char* fdns_last_error(void);
+
+/* ABI version, for the host loader's sanity check. */
+int32_t fdns_abi_version(void);
+
+/* Number of hot-path kernels this library has launched so far (all
+ * threads); the bench reports the delta over its timed region. */
+int64_t fdns_launch_count(void);
+
+/* Number of work arrays a variant allocates (plan.py:220-227: BL 60 (+0
+ * scratch -- products are formed in registers), RA/SN 0, RS/SS 9). */
+int32_t fdns_workarray_count(int32_t variant);
+
+/* Primitive recovery u, p, T from the conservative fields of a state bundle,
+ * over the full padded arrays -- replaces eval_primitives_fused /
+ * eval_primitives_grouped (physics.py:169-202). */
+int32_t fdns_primitives(double* state, const fdns_problem* pb, void* stream);
+
+/* Periodic ghost fill of nf consecutive fields along the axes in axes_mask
+ * (bit a = axis a) -- replaces mesh.halo_exchange (mesh.py:118-139). */
+int32_t fdns_halo_wrap(double* fields, int32_t nf, int32_t axes_mask,
+                       const fdns_problem* pb, void* stream);
+
+/* Residual of a state bundle (primitives and halos current) under a variant;
+ * writes the interior of the 5 residual fields -- replaces
+ * ResidualEvaluator.evaluate (plan.py:394-416) and the generated kernel
+ * (codegen.py:156-179).  `work` holds fdns_workarray_count(variant) padded
+ * fields (may be NULL when the count is 0). */
+int32_t fdns_residual(int32_t variant, const double* state, double* work,
+                      double* out, const fdns_problem* pb, void* stream);
+
+/* RK stage update cons = saved + coef*res on the interior of 5 fields --
+ * replaces the update loop of rk_substep (timeloop.py:80-85). */
+int32_t fdns_rk_update(double* cons, const double* saved, const double* res,
+                       double coef, const fdns_problem* pb, void* stream);
+
+/* One fused RK stage: residual of `in` (a state bundle with current halos)
+ * under the variant, q = saved + coef*R, primitives of q, all written to the
+ * interior of the `out` state bundle (halos are left to fdns_halo_wrap / the
+ * slab exchange).  `saved` is 5 conservative fields and may alias `out`
+ * (pointwise update).  Bitwise equal to fdns_residual + fdns_rk_update +
+ * fdns_primitives -- replaces rk_substep (timeloop.py:75-85). */
+int32_t fdns_stage(int32_t variant, const double* in, const double* saved,
+                   double* out, double* work, double coef,
+                   const fdns_problem* pb, void* stream);
+
+/* Device reduction of the diagnostics of a state bundle (halos current):
+ * out[0] = sum 0.5*rho*|u|^2, out[1] = sum 0.5*rho*|omega|^2,
+ * out[2..6] = interior sums of rho, rhou0..2, rhoE, out[7] = count of
+ * non-finite conservative values, out[8] = count of rho <= 0.
+ * `partials` is scratch of fdns_diag_partials_size() doubles.  Replaces
+ * kinetic_energy_integral / enstrophy_integral / conservation_sums /
+ * check_physical (diagnostics.py:94-146, physics.py:121-129). */
+int32_t fdns_diag_partials_size(const fdns_problem* pb);
+int32_t fdns_reduce_diag(const double* state, double* partials, double* out9,
+                         const fdns_problem* pb, void* stream);
+
+/* FP64 issue-rate probe: runs a DADD-only kernel for `iters` iterations and
+ * returns (via out[0]) the number of FP64 instructions it executed; time it
+ * with events on `stream` to get the in-run FP64 peak for the roofline. */
+int32_t fdns_fp64_probe(double* scratch, int32_t iters, double* out_count,
+                        void* stream);
+
+/* L2 flush helper for timing hygiene: writes `bytes` of `buf`. */
+int32_t fdns_l2_flush(void* buf, int64_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDNS_B200_H */

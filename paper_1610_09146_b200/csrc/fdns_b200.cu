@@ -1,0 +1,553 @@
+// fdns_b200.cu -- sm_100a kernels and the C ABI (include/fdns_b200.h).
+//
+// Built with -fmad=false (no FMA contraction) and IEEE division so every
+// kernel reproduces the reference's bits (see fdns_math.cuh).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/fdns_b200.h"
+#include "fdns_math.cuh"
+
+
+using namespace fdns;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+inline void count(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int fail(const char* what, cudaError_t e) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return 1;
+}
+int fail(const std::string& what) {
+  g_err = what;
+  return 2;
+}
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(what, e);
+  return 0;
+}
+
+Coef make_coef(const fdns_problem* pb) {
+  Coef k;
+  for (int a = 0; a < 3; ++a) {
+    k.w1[a] = pb->w[5 * a + 0];
+    k.w2[a] = pb->w[5 * a + 1];
+    k.s0[a] = pb->w[5 * a + 2];
+    k.s1[a] = pb->w[5 * a + 3];
+    k.s2[a] = pb->w[5 * a + 4];
+  }
+  k.inv_Re = pb->kc[0];
+  k.c13 = pb->kc[1];
+  k.c43 = pb->kc[2];
+  k.c23 = pb->kc[3];
+  k.heat = pb->kc[4];
+  k.gm1 = pb->gm1;
+  k.gM2 = pb->gM2;
+  return k;
+}
+
+Geom make_geom(const fdns_problem* pb) {
+  Geom g;
+  g.n0 = pb->n[0];
+  g.n1 = pb->n[1];
+  g.n2 = pb->n[2];
+  g.h = pb->h;
+  const int64_t P1 = g.n1 + 2 * g.h, P2 = g.n2 + 2 * g.h;
+  g.s1 = P2;
+  g.s0 = P1 * P2;
+  g.fs = (int64_t)(g.n0 + 2 * g.h) * g.s0;
+  return g;
+}
+
+int validate(const fdns_problem* pb) {
+  if (!pb) return fail("null problem");
+  if (pb->h < 2) return fail("halo width must be >= 2");
+  for (int a = 0; a < 3; ++a)
+    if (pb->n[a] < 1) return fail("interior extent must be positive");
+  if (pb->n[1] < pb->h || pb->n[2] < pb->h) return fail("axes 1/2 need at least h points");
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Primitives over the full padded bundle
+// ---------------------------------------------------------------------------
+__global__ void k_primitives(double* __restrict__ F, Coef k, int64_t fs) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < fs;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    double q[5], pr[5];
+#pragma unroll
+    for (int f = 0; f < 5; ++f) q[f] = F[f * fs + c];
+    primitives_point(k, q, pr);
+#pragma unroll
+    for (int f = 0; f < 5; ++f) F[(5 + f) * fs + c] = pr[f];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Periodic ghost fill (mesh.py:118-139).  After the reference's axis-ordered
+// full-slab copies every ghost holds the interior value at the coordinates
+// wrapped on each exchanged axis; this kernel writes exactly that, visiting
+// only ghost points (three disjoint regions).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int wrap(int x, int n, int h) {
+  return x < h ? x + n : (x >= n + h ? x - n : x);
+}
+
+__global__ void k_halo_wrap(double* __restrict__ F, int nf, int mask, Geom g, int64_t r0,
+                            int64_t r1, int64_t r2) {
+  const int h = g.h;
+  const int P0 = g.n0 + 2 * h, P1 = g.n1 + 2 * h, P2 = g.n2 + 2 * h;
+  const bool m0 = mask & 1, m1 = mask & 2, m2 = mask & 4;
+  const int64_t total = r0 + r1 + r2;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int i, j, k;
+    if (t < r0) {  // axis-0 ghost planes, all j, k
+      int64_t u = t;
+      k = u % P2; u /= P2;
+      j = u % P1; u /= P1;
+      i = (int)u;  // 0 .. 2h-1
+      i = i < h ? i : g.n0 + i;
+    } else if (t < r0 + r1) {  // axis-1 ghosts
+      int64_t u = t - r0;
+      const int ni = m0 ? g.n0 : P0;
+      k = u % P2; u /= P2;
+      j = u % (2 * h); u /= (2 * h);
+      i = (int)u + (m0 ? h : 0);
+      (void)ni;
+      j = j < h ? j : g.n1 + j;
+    } else {  // axis-2 ghosts
+      int64_t u = t - r0 - r1;
+      const int nj = m1 ? g.n1 : P1;
+      k = u % (2 * h); u /= (2 * h);
+      j = (int)(u % nj) + (m1 ? h : 0); u /= nj;
+      i = (int)u + (m0 ? h : 0);
+      k = k < h ? k : g.n2 + k;
+    }
+    const int si = m0 ? wrap(i, g.n0, h) : i;
+    const int sj = m1 ? wrap(j, g.n1, h) : j;
+    const int sk = m2 ? wrap(k, g.n2, h) : k;
+    const int64_t dst = i * g.s0 + j * g.s1 + k;
+    const int64_t src = si * g.s0 + sj * g.s1 + sk;
+    for (int f = 0; f < nf; ++f) F[f * g.fs + dst] = F[f * g.fs + src];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Point-kernel residual (one thread per interior point), all variants.
+// Mode: 0 = write residual, 1 = fused RK update + primitives.
+// ---------------------------------------------------------------------------
+template <int V>
+struct VariantTag {};
+
+template <int V, int MODE>
+__global__ void __launch_bounds__(256) k_residual(const double* __restrict__ in,
+                                                  const double* saved, double* out,
+                                                  const double* __restrict__ work, Coef k,
+                                                  Geom g, double coef) {
+  const int kk = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
+  const int ii = blockIdx.z;
+  if (kk >= g.n2 || jj >= g.n1) return;
+  const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
+  double r[NFIELDS];
+#pragma unroll
+  for (int f = 0; f < NFIELDS; ++f) r[f] = __ldg(in + f * g.fs + c);
+  double R[5];
+  if constexpr (V == FDNS_SN) {
+    GAcc a{in, c, g.s0, g.s1, g.fs};
+    LocalProvider<GAcc> P(k, a);
+    residual_point(k, P, r, R);
+  } else if constexpr (V == FDNS_RA) {
+    VAcc a{in, c, g.s0, g.s1, g.fs};
+    InlineProvider<VAcc> P(k, a);
+    residual_point(k, P, r, R);
+  } else if constexpr (V == FDNS_BL) {
+    FetchProvider P{work, c, g.fs};
+    residual_point(k, P, r, R);
+  } else if constexpr (V == FDNS_SS) {
+    GAcc a{in, c, g.s0, g.s1, g.fs};
+    SSProvider<GAcc> P(k, a, work, c, g.fs, g.s0, g.s1);
+    residual_point(k, P, r, R);
+  } else {  // RS: stored velocity gradients, everything else inline
+    VAcc a{in, c, g.s0, g.s1, g.fs};
+    SSProvider<VAcc> P(k, a, work, c, g.fs, g.s0, g.s1);
+    residual_point(k, P, r, R);
+  }
+  if constexpr (MODE == 0) {
+#pragma unroll
+    for (int f = 0; f < 5; ++f) out[f * g.fs + c] = R[f];
+  } else {
+    double q[5], pr[5];
+#pragma unroll
+    for (int f = 0; f < 5; ++f) q[f] = saved[f * g.fs + c] + coef * R[f];
+    primitives_point(k, q, pr);
+#pragma unroll
+    for (int f = 0; f < 5; ++f) out[f * g.fs + c] = q[f];
+#pragma unroll
+    for (int f = 0; f < 5; ++f) out[(5 + f) * g.fs + c] = pr[f];
+  }
+}
+
+// BL fill: the 54 plain/product derivatives of every interior point into
+// their work arrays (plan.py:369-392; products formed per point, bitwise
+// equal to the scratch route).  The diagonal velocity gradients are written
+// by k_diag_ext over the extended region instead.
+template <int A_, int L>
+__device__ __forceinline__ void fill_axis(const Coef& k, const GAcc& a, double* __restrict__ wa,
+                                          int64_t fs) {
+  if constexpr (!(L >= S_U && L < S_U + 3 && (L - S_U) == A_))
+    wa[slot(A_, L) * fs + a.c] = eval_slot<A_, L>(k, a);
+  if constexpr (L + 1 < S_PER_AXIS) fill_axis<A_, L + 1>(k, a, wa, fs);
+}
+
+template <int A_>
+__global__ void __launch_bounds__(256) k_fill_bl(const double* __restrict__ in,
+                                                 double* __restrict__ wa, Coef k, Geom g) {
+  const int kk = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
+  const int ii = blockIdx.z;
+  if (kk >= g.n2 || jj >= g.n1) return;
+  const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
+  GAcc a{in, c, g.s0, g.s1, g.fs};
+  fill_axis<A_, 0>(k, a, wa, g.fs);
+}
+
+// Diagonal velocity gradients D(u_q, x_q) on every point whose axis-q
+// coordinate is interior (other axes over the full padded range): exactly the
+// values the reference's halo-exchanged inner arrays hold (plan.py:378-379),
+// computed redundantly instead of exchanged, so slab ranks need no second
+// exchange.  dst[q] is the array for D(u_q, x_q).
+__global__ void k_diag_ext(const double* __restrict__ in, double* d0, double* d1p, double* d2p,
+                           Coef k, Geom g) {
+  const int h = g.h;
+  const int P1 = g.n1 + 2 * h, P2 = g.n2 + 2 * h;
+  const int64_t total = g.fs;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < total;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int kq = c % P2;
+    const int jq = (c / P2) % P1;
+    const int iq = c / g.s0;
+    const bool in0 = iq >= h && iq < g.n0 + h;
+    const bool in1 = jq >= h && jq < g.n1 + h;
+    const bool in2 = kq >= h && kq < g.n2 + h;
+    GAcc a{in, c, g.s0, g.s1, g.fs};
+    if (in0) d0[c] = d1<0, E_FIELD, U0, 0>(k, a);
+    if (in1) d1p[c] = d1<1, E_FIELD, U1, 0>(k, a);
+    if (in2) d2p[c] = d1<2, E_FIELD, U2, 0>(k, a);
+  }
+}
+
+// BL mixed fills: outer derivative of the stored inner arrays (plan.py:380-382).
+__global__ void __launch_bounds__(256) k_fill_cross(double* __restrict__ wa, Coef k, Geom g) {
+  const int kk = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
+  const int ii = blockIdx.z;
+  if (kk >= g.n2 || jj >= g.n1) return;
+  const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
+  const int64_t st[3] = {g.s0, g.s1, 1};
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const double* inner = wa + slot(j, S_U + j) * g.fs;
+#pragma unroll
+    for (int o = 0; o < 3; ++o) {
+      if (o == j) continue;
+      wa[(S_DD + dd_index(j, o)) * g.fs + c] = d1_stored(k, o, inner, c, st[o]);
+    }
+  }
+}
+
+// SS/RS fill: the six off-diagonal velocity gradients on the interior
+// (diagonals come from k_diag_ext).  ws[q*3+a] = D(u_q, x_a).
+__global__ void __launch_bounds__(256) k_grad_ss(const double* __restrict__ in,
+                                                 double* __restrict__ ws, Coef k, Geom g) {
+  const int kk = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
+  const int ii = blockIdx.z;
+  if (kk >= g.n2 || jj >= g.n1) return;
+  const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
+  GAcc a{in, c, g.s0, g.s1, g.fs};
+  ws[(0 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U0, 0>(k, a);
+  ws[(0 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U0, 0>(k, a);
+  ws[(1 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U1, 0>(k, a);
+  ws[(1 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U1, 0>(k, a);
+  ws[(2 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U2, 0>(k, a);
+  ws[(2 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U2, 0>(k, a);
+}
+
+// RK update on the interior of 5 fields (timeloop.py:80-85).
+__global__ void k_rk_update(double* cons, const double* saved, const double* __restrict__ res,
+                            double coef, Geom g) {
+  const int kk = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
+  const int ii = blockIdx.z;
+  if (kk >= g.n2 || jj >= g.n1) return;
+  const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
+#pragma unroll
+  for (int f = 0; f < 5; ++f) cons[f * g.fs + c] = saved[f * g.fs + c] + coef * res[f * g.fs + c];
+}
+
+// ---------------------------------------------------------------------------
+// Diagnostics reduction (diagnostics.py:89-146, physics.py:121-129).
+// Deterministic: fixed grid, fixed per-thread order, fixed tree.
+// ---------------------------------------------------------------------------
+constexpr int DIAG_Q = 9;
+constexpr int DIAG_THREADS = 256;
+constexpr int DIAG_BLOCKS = 148 * 4;
+
+__global__ void __launch_bounds__(DIAG_THREADS) k_diag(const double* __restrict__ in,
+                                                        double* __restrict__ partials, Coef k,
+                                                        Geom g) {
+  double acc[DIAG_Q];
+#pragma unroll
+  for (int q = 0; q < DIAG_Q; ++q) acc[q] = 0.0;
+  const int64_t npts = (int64_t)g.n0 * g.n1 * g.n2;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < npts;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int kk = t % g.n2;
+    const int jj = (t / g.n2) % g.n1;
+    const int ii = t / ((int64_t)g.n1 * g.n2);
+    const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
+    GAcc a{in, c, g.s0, g.s1, g.fs};
+    const double rho = a.v(RHO, 0, 0, 0);
+    const double u0 = a.v(U0, 0, 0, 0), u1 = a.v(U1, 0, 0, 0), u2 = a.v(U2, 0, 0, 0);
+    acc[0] += 0.5 * rho * (u0 * u0 + u1 * u1 + u2 * u2);
+    const double w0 = d1<1, E_FIELD, U2, 0>(k, a) - d1<2, E_FIELD, U1, 0>(k, a);
+    const double w1 = d1<2, E_FIELD, U0, 0>(k, a) - d1<0, E_FIELD, U2, 0>(k, a);
+    const double w2 = d1<0, E_FIELD, U1, 0>(k, a) - d1<1, E_FIELD, U0, 0>(k, a);
+    acc[1] += 0.5 * rho * (w0 * w0 + w1 * w1 + w2 * w2);
+#pragma unroll
+    for (int f = 0; f < 5; ++f) {
+      const double v = a.v(f, 0, 0, 0);
+      acc[2 + f] += v;
+      if (!isfinite(v)) acc[7] += 1.0;
+    }
+    if (!(rho > 0.0)) acc[8] += 1.0;
+  }
+  __shared__ double sh[DIAG_Q][DIAG_THREADS];
+#pragma unroll
+  for (int q = 0; q < DIAG_Q; ++q) sh[q][threadIdx.x] = acc[q];
+  __syncthreads();
+  for (int s = DIAG_THREADS / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+#pragma unroll
+      for (int q = 0; q < DIAG_Q; ++q) sh[q][threadIdx.x] += sh[q][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x < DIAG_Q) partials[blockIdx.x * DIAG_Q + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+__global__ void k_diag_final(const double* __restrict__ partials, int nblocks, double* out) {
+  __shared__ double sh[DIAG_Q][256];
+  double acc[DIAG_Q];
+  for (int q = 0; q < DIAG_Q; ++q) acc[q] = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x)
+    for (int q = 0; q < DIAG_Q; ++q) acc[q] += partials[b * DIAG_Q + q];
+  for (int q = 0; q < DIAG_Q; ++q) sh[q][threadIdx.x] = acc[q];
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int q = 0; q < DIAG_Q; ++q) sh[q][threadIdx.x] += sh[q][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x < DIAG_Q) out[threadIdx.x] = sh[threadIdx.x][0];
+}
+
+// FP64 issue-rate probe: 8 independent DADD chains per thread.
+constexpr int PROBE_BLOCKS = 148 * 8, PROBE_THREADS = 256, PROBE_CHAINS = 8;
+__global__ void __launch_bounds__(PROBE_THREADS) k_fp64_probe(double* out, int iters, double y) {
+  double x[PROBE_CHAINS];
+#pragma unroll
+  for (int c = 0; c < PROBE_CHAINS; ++c) x[c] = threadIdx.x * 1e-3 + c;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < PROBE_CHAINS; ++c) x[c] = x[c] + y;
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < PROBE_CHAINS; ++c) s += x[c];
+  if (s == 123.456) out[0] = s;  // keep the chains live
+}
+
+__global__ void k_l2_flush(uint4* buf, int64_t n, uint32_t v) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    buf[t] = make_uint4(v, v + 1, v + 2, v + 3);
+}
+
+inline dim3 point_grid(const Geom& g, dim3 blk) {
+  return dim3((g.n2 + blk.x - 1) / blk.x, (g.n1 + blk.y - 1) / blk.y, g.n0);
+}
+
+template <int MODE>
+int launch_residual(int variant, const double* in, const double* saved, double* out,
+                    double* work, const Coef& k, const Geom& g, double coef, cudaStream_t s) {
+  const dim3 blk(32, 8, 1);
+  const dim3 grd = point_grid(g, blk);
+  switch (variant) {
+    case FDNS_BL: k_residual<FDNS_BL, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef); break;
+    case FDNS_RA: k_residual<FDNS_RA, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef); break;
+    case FDNS_RS: k_residual<FDNS_RS, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef); break;
+    case FDNS_SN: k_residual<FDNS_SN, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef); break;
+    case FDNS_SS: k_residual<FDNS_SS, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef); break;
+    default: return fail("unknown variant");
+  }
+  count();
+  return check_launch("residual kernel");
+}
+
+// Work-array fills that precede the residual kernel (BL, RS, SS).
+int launch_fills(int variant, const double* in, double* work, const Coef& k, const Geom& g,
+                 cudaStream_t s) {
+  const dim3 blk(32, 8, 1);
+  const dim3 grd = point_grid(g, blk);
+  const int ext_blocks = (int)std::min<int64_t>((g.fs + 255) / 256, 148 * 16);
+  if (variant == FDNS_BL) {
+    k_fill_bl<0><<<grd, blk, 0, s>>>(in, work, k, g);
+    k_fill_bl<1><<<grd, blk, 0, s>>>(in, work, k, g);
+    k_fill_bl<2><<<grd, blk, 0, s>>>(in, work, k, g);
+    k_diag_ext<<<ext_blocks, 256, 0, s>>>(in, work + slot(0, S_U + 0) * g.fs,
+                                          work + slot(1, S_U + 1) * g.fs,
+                                          work + slot(2, S_U + 2) * g.fs, k, g);
+    k_fill_cross<<<grd, blk, 0, s>>>(work, k, g);
+    count(5);
+    return check_launch("BL fills");
+  }
+  if (variant == FDNS_SS || variant == FDNS_RS) {
+    k_grad_ss<<<grd, blk, 0, s>>>(in, work, k, g);
+    k_diag_ext<<<ext_blocks, 256, 0, s>>>(in, work + 0 * g.fs, work + 4 * g.fs, work + 8 * g.fs,
+                                          k, g);
+    count(2);
+    return check_launch("SS fills");
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* fdns_last_error(void) { return g_err.c_str(); }
+
+int32_t fdns_abi_version(void) { return 1; }
+
+int64_t fdns_launch_count(void) { return g_launches.load(); }
+
+int32_t fdns_workarray_count(int32_t variant) {
+  switch (variant) {
+    case FDNS_BL: return N_SLOTS;
+    case FDNS_RS:
+    case FDNS_SS: return 9;
+    case FDNS_RA:
+    case FDNS_SN: return 0;
+    default: return -1;
+  }
+}
+
+int32_t fdns_primitives(double* state, const fdns_problem* pb, void* stream) {
+  if (int e = validate(pb)) return e;
+  const Geom g = make_geom(pb);
+  const Coef k = make_coef(pb);
+  const int blocks = (int)std::min<int64_t>((g.fs + 255) / 256, 148 * 16);
+  k_primitives<<<blocks, 256, 0, (cudaStream_t)stream>>>(state, k, g.fs);
+  count();
+  return check_launch("primitives kernel");
+}
+
+int32_t fdns_halo_wrap(double* fields, int32_t nf, int32_t axes_mask, const fdns_problem* pb,
+                       void* stream) {
+  if (int e = validate(pb)) return e;
+  const Geom g = make_geom(pb);
+  const int h = g.h;
+  const int64_t P0 = g.n0 + 2 * h, P1 = g.n1 + 2 * h, P2 = g.n2 + 2 * h;
+  const bool m0 = axes_mask & 1, m1 = axes_mask & 2, m2 = axes_mask & 4;
+  if (m0 && g.n0 < h) return fail("axis 0 needs at least h points to wrap");
+  const int64_t r0 = m0 ? 2 * h * P1 * P2 : 0;
+  const int64_t r1 = m1 ? (m0 ? g.n0 : P0) * 2 * h * P2 : 0;
+  const int64_t r2 = m2 ? (m0 ? g.n0 : P0) * (m1 ? g.n1 : P1) * 2 * h : 0;
+  const int64_t total = r0 + r1 + r2;
+  if (total == 0 || nf == 0) return 0;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_halo_wrap<<<blocks, 256, 0, (cudaStream_t)stream>>>(fields, nf, axes_mask, g, r0, r1, r2);
+  count();
+  return check_launch("halo wrap kernel");
+}
+
+int32_t fdns_residual(int32_t variant, const double* state, double* work, double* out,
+                      const fdns_problem* pb, void* stream) {
+  if (int e = validate(pb)) return e;
+  const int nw = fdns_workarray_count(variant);
+  if (nw < 0) return fail("unknown variant");
+  if (nw > 0 && !work) return fail("variant needs work arrays");
+  const Geom g = make_geom(pb);
+  const Coef k = make_coef(pb);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int e = launch_fills(variant, state, work, k, g, s)) return e;
+  return launch_residual<0>(variant, state, nullptr, out, work, k, g, 0.0, s);
+}
+
+int32_t fdns_rk_update(double* cons, const double* saved, const double* res, double coef,
+                       const fdns_problem* pb, void* stream) {
+  if (int e = validate(pb)) return e;
+  const Geom g = make_geom(pb);
+  const dim3 blk(32, 8, 1);
+  k_rk_update<<<point_grid(g, blk), blk, 0, (cudaStream_t)stream>>>(cons, saved, res, coef, g);
+  count();
+  return check_launch("rk update kernel");
+}
+
+int32_t fdns_stage(int32_t variant, const double* in, const double* saved, double* out,
+                   double* work, double coef, const fdns_problem* pb, void* stream) {
+  if (int e = validate(pb)) return e;
+  const int nw = fdns_workarray_count(variant);
+  if (nw < 0) return fail("unknown variant");
+  if (nw > 0 && !work) return fail("variant needs work arrays");
+  if (in == out) return fail("fused stage needs distinct in/out bundles");
+  const Geom g = make_geom(pb);
+  const Coef k = make_coef(pb);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int e = launch_fills(variant, in, work, k, g, s)) return e;
+  return launch_residual<1>(variant, in, saved, out, work, k, g, coef, s);
+}
+
+int32_t fdns_diag_partials_size(const fdns_problem*) { return DIAG_BLOCKS * DIAG_Q; }
+
+int32_t fdns_reduce_diag(const double* state, double* partials, double* out9,
+                         const fdns_problem* pb, void* stream) {
+  if (int e = validate(pb)) return e;
+  const Geom g = make_geom(pb);
+  const Coef k = make_coef(pb);
+  cudaStream_t s = (cudaStream_t)stream;
+  k_diag<<<DIAG_BLOCKS, DIAG_THREADS, 0, s>>>(state, partials, k, g);
+  k_diag_final<<<1, 256, 0, s>>>(partials, DIAG_BLOCKS, out9);
+  count(2);
+  return check_launch("diagnostics kernels");
+}
+
+int32_t fdns_fp64_probe(double* scratch, int32_t iters, double* out_count, void* stream) {
+  k_fp64_probe<<<PROBE_BLOCKS, PROBE_THREADS, 0, (cudaStream_t)stream>>>(scratch, iters, 1e-9);
+  if (out_count)
+    *out_count = (double)PROBE_BLOCKS * PROBE_THREADS * (double)iters * PROBE_CHAINS;
+  return check_launch("fp64 probe");
+}
+
+int32_t fdns_l2_flush(void* buf, int64_t bytes, void* stream) {
+  const int64_t n = bytes / 16;
+  static uint32_t v = 1;
+  k_l2_flush<<<148 * 8, 256, 0, (cudaStream_t)stream>>>((uint4*)buf, n, v++);
+  return check_launch("l2 flush");
+}
+
+}  // extern "C"

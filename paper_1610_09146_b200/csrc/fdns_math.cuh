@@ -1,0 +1,326 @@
+// fdns_math.cuh -- per-point arithmetic of the 4th-order compressible
+// Navier-Stokes residual, shared by every variant kernel.
+//
+// The arithmetic contract is the reference term list
+// (pkg/src/fdns/terms.py:135-200) with the stencil shapes of
+// pkg/src/fdns/stencil.py:71-102 / codegen.py:81-102.  Every expression below
+// keeps the reference's left-to-right association, and the library is built
+// with -fmad=false and IEEE division, so each variant reproduces the
+// reference bits exactly (parity gate: tests/test_gpu_parity.py).
+//
+// The derivative *provider* decides where a derivative value comes from,
+// which is exactly what distinguishes the paper's variants:
+//   LocalProvider   (SN)  every distinct derivative evaluated once, kept live
+//   InlineProvider  (RA)  re-expanded from the stencil at every occurrence
+//   FetchProvider   (BL)  read from a stored work array
+//   SSProvider      (SS)  9 velocity gradients stored, the rest local
+// The residual body (residual_point) is written once over the provider API.
+#pragma once
+#include <cstdint>
+
+namespace fdns {
+
+enum Fld : int { RHO = 0, RU0, RU1, RU2, RHOE_F, U0, U1, U2, PF, TF, NFIELDS };
+
+// Stencil weights per axis, pre-divided by the spacing (stencil.py:45-51),
+// plus the five kernel constants (physics.py:78-81) and gm1/gM2.
+struct Coef {
+  double w1[3], w2[3], s0[3], s1[3], s2[3];
+  double inv_Re, c13, c43, c23, heat;
+  double gm1, gM2;
+};
+
+// Geometry of one padded bundle: field stride fs and axis strides.
+struct Geom {
+  int n0, n1, n2, h;   // interior points per axis (n0 = local slab planes)
+  int64_t s0, s1, fs;  // strides (elements) of axis 0, axis 1, field
+};
+
+// ---------------------------------------------------------------------------
+// Point accessors: value of field f at the centre point shifted by (di,dj,dk)
+// ---------------------------------------------------------------------------
+
+// Global-memory accessor through the read-only path.  Loads may be merged by
+// the compiler (used by LOCAL/FETCH providers).
+struct GAcc {
+  const double* __restrict__ b;
+  int64_t c, s0, s1, fs;
+  __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
+    return __ldg(b + f * fs + c + di * s0 + dj * s1 + dk);
+  }
+};
+
+// Global-memory accessor whose loads are volatile, so the compiler can merge
+// neither the loads nor the arithmetic built on them: every occurrence of a
+// derivative is genuinely recomputed (RA semantics, plan.py:172-173).
+struct VAcc {
+  const double* b;
+  int64_t c, s0, s1, fs;
+  __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
+    const double* p = b + f * fs + c + di * s0 + dj * s1 + dk;
+    double r;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Point expressions of the term list (terms.py:39, :158-174)
+// ---------------------------------------------------------------------------
+template <int AX> struct Off {
+  static __device__ __forceinline__ void at(int o, int& di, int& dj, int& dk) {
+    di = AX == 0 ? o : 0; dj = AX == 1 ? o : 0; dk = AX == 2 ? o : 0;
+  }
+};
+
+template <class A>
+__device__ __forceinline__ double rhoe_at(const A& a, int di, int dj, int dk) {
+  return a.v(RHOE_F, di, dj, dk) -
+         0.5 * (a.v(RU0, di, dj, dk) * a.v(U0, di, dj, dk) +
+                a.v(RU1, di, dj, dk) * a.v(U1, di, dj, dk) +
+                a.v(RU2, di, dj, dk) * a.v(U2, di, dj, dk));
+}
+
+// Expression kinds differentiated by the stencils.
+enum Ex : int { E_FIELD = 0, E_PROD, E_RHOE, E_RHOEU };
+
+template <int EX, int F, int G, class A>
+__device__ __forceinline__ double ex_at(const A& a, int di, int dj, int dk) {
+  if constexpr (EX == E_FIELD) return a.v(F, di, dj, dk);
+  else if constexpr (EX == E_PROD) return a.v(F, di, dj, dk) * a.v(G, di, dj, dk);
+  else if constexpr (EX == E_RHOE) return rhoe_at(a, di, dj, dk);
+  else return rhoe_at(a, di, dj, dk) * a.v(G, di, dj, dk);
+}
+
+// First derivative along AX of expression EX at centre+(bi,bj,bk):
+//   fw1*((e(+1)) - (e(-1))) + fw2*((e(+2)) - (e(-2)))   (stencil.py:80-84)
+template <int AX, int EX, int F, int G, class A>
+__device__ __forceinline__ double d1(const Coef& k, const A& a, int bi = 0,
+                                     int bj = 0, int bk = 0) {
+  int i1, j1, k1;
+  Off<AX>::at(1, i1, j1, k1);
+  const double ep1 = ex_at<EX, F, G>(a, bi + i1, bj + j1, bk + k1);
+  const double em1 = ex_at<EX, F, G>(a, bi - i1, bj - j1, bk - k1);
+  const double ep2 = ex_at<EX, F, G>(a, bi + 2 * i1, bj + 2 * j1, bk + 2 * k1);
+  const double em2 = ex_at<EX, F, G>(a, bi - 2 * i1, bj - 2 * j1, bk - 2 * k1);
+  return k.w1[AX] * (ep1 - em1) + k.w2[AX] * (ep2 - em2);
+}
+
+// Second derivative along AX of field F (stencil.py:97-101).
+template <int AX, int F, class A>
+__device__ __forceinline__ double d2(const Coef& k, const A& a) {
+  int i1, j1, k1;
+  Off<AX>::at(1, i1, j1, k1);
+  return k.s0[AX] * a.v(F, 0, 0, 0) +
+         k.s1[AX] * (a.v(F, i1, j1, k1) + a.v(F, -i1, -j1, -k1)) +
+         k.s2[AX] * (a.v(F, 2 * i1, 2 * j1, 2 * k1) + a.v(F, -2 * i1, -2 * j1, -2 * k1));
+}
+
+// Mixed DD(u_J, x_O, x_J): outer first derivative along O of the inner first
+// derivative D(u_J, x_J) re-expanded at the four shifted points
+// (codegen.py:97-102).
+template <int O, int J, class A>
+__device__ __forceinline__ double dd(const Coef& k, const A& a) {
+  int i1, j1, k1;
+  Off<O>::at(1, i1, j1, k1);
+  const double ip1 = d1<J, E_FIELD, U0 + J, 0>(k, a, i1, j1, k1);
+  const double im1 = d1<J, E_FIELD, U0 + J, 0>(k, a, -i1, -j1, -k1);
+  const double ip2 = d1<J, E_FIELD, U0 + J, 0>(k, a, 2 * i1, 2 * j1, 2 * k1);
+  const double im2 = d1<J, E_FIELD, U0 + J, 0>(k, a, -2 * i1, -2 * j1, -2 * k1);
+  return k.w1[O] * (ip1 - im1) + k.w2[O] * (ip2 - im2);
+}
+
+// Outer first derivative along O of a stored inner-derivative array (the
+// reference's FETCH inner read, codegen.py:111-113).
+__device__ __forceinline__ double d1_stored(const Coef& k, int O,
+                                            const double* __restrict__ wa,
+                                            int64_t c, int64_t s) {
+  return k.w1[O] * (__ldg(wa + c + s) - __ldg(wa + c - s)) +
+         k.w2[O] * (__ldg(wa + c + 2 * s) - __ldg(wa + c - 2 * s));
+}
+
+// ---------------------------------------------------------------------------
+// Derivative slots (60 distinct derivatives, terms.py:135-200)
+// per axis a: 18 slots at a*18 + ...; then 6 mixed at 54 + ...
+// ---------------------------------------------------------------------------
+enum Slot : int {
+  S_RHO = 0, S_P, S_RHOE, S_RHOEU, S_UP, S_T2,
+  S_RU = 6,    // + q        D(rhou_q, x_a)
+  S_U = 9,     // + q        D(u_q, x_a)
+  S_RUU = 12,  // + q        D(rhou_q * u_a, x_a)
+  S_U2 = 15,   // + q        D2(u_q, x_a)
+  S_PER_AXIS = 18,
+  S_DD = 54,   // + dd_index(j, o)   DD(u_j, x_o, x_j)
+  N_SLOTS = 60
+};
+__host__ __device__ constexpr int slot(int a, int local) { return a * S_PER_AXIS + local; }
+// mixed index for (inner field j, outer axis o), o != j
+__host__ __device__ constexpr int dd_index(int j, int o) { return j * 2 + (o < j ? o : o - 1); }
+
+// Evaluate one derivative slot from point data (used by LOCAL/INLINE
+// providers and by the BL fill kernels).
+template <int A_, int L, class Acc>
+__device__ __forceinline__ double eval_slot(const Coef& k, const Acc& a) {
+  if constexpr (L == S_RHO) return d1<A_, E_FIELD, RHO, 0>(k, a);
+  else if constexpr (L == S_P) return d1<A_, E_FIELD, PF, 0>(k, a);
+  else if constexpr (L == S_RHOE) return d1<A_, E_RHOE, 0, 0>(k, a);
+  else if constexpr (L == S_RHOEU) return d1<A_, E_RHOEU, 0, U0 + A_>(k, a);
+  else if constexpr (L == S_UP) return d1<A_, E_PROD, U0 + A_, PF>(k, a);
+  else if constexpr (L == S_T2) return d2<A_, TF>(k, a);
+  else if constexpr (L >= S_RU && L < S_RU + 3) return d1<A_, E_FIELD, RU0 + (L - S_RU), 0>(k, a);
+  else if constexpr (L >= S_U && L < S_U + 3) return d1<A_, E_FIELD, U0 + (L - S_U), 0>(k, a);
+  else if constexpr (L >= S_RUU && L < S_RUU + 3) return d1<A_, E_PROD, RU0 + (L - S_RUU), U0 + A_>(k, a);
+  else return d2<A_, U0 + (L - S_U2)>(k, a);
+}
+
+// ---------------------------------------------------------------------------
+// Providers
+// ---------------------------------------------------------------------------
+
+// INLINE (RA): every call re-expands the stencil.
+template <class Acc>
+struct InlineProvider {
+  const Coef& k;
+  const Acc& a;
+  __device__ InlineProvider(const Coef& k_, const Acc& a_) : k(k_), a(a_) {}
+  template <int A_, int L> __device__ __forceinline__ double g() const { return eval_slot<A_, L>(k, a); }
+  template <int J, int O> __device__ __forceinline__ double x() const { return dd<O, J>(k, a); }
+};
+
+// LOCAL (SN): each distinct derivative evaluated once into a local.
+template <class Acc>
+struct LocalProvider {
+  double v[N_SLOTS];
+  template <int A_, int L> __device__ __forceinline__ void fill1(const Coef& k, const Acc& a) {
+    v[slot(A_, L)] = eval_slot<A_, L>(k, a);
+    if constexpr (L + 1 < S_PER_AXIS) fill1<A_, L + 1>(k, a);
+  }
+  __device__ __forceinline__ LocalProvider(const Coef& k, const Acc& a) {
+    fill1<0, 0>(k, a);
+    fill1<1, 0>(k, a);
+    fill1<2, 0>(k, a);
+    v[S_DD + dd_index(1, 0)] = dd<0, 1>(k, a);
+    v[S_DD + dd_index(2, 0)] = dd<0, 2>(k, a);
+    v[S_DD + dd_index(0, 1)] = dd<1, 0>(k, a);
+    v[S_DD + dd_index(2, 1)] = dd<1, 2>(k, a);
+    v[S_DD + dd_index(0, 2)] = dd<2, 0>(k, a);
+    v[S_DD + dd_index(1, 2)] = dd<2, 1>(k, a);
+  }
+  template <int A_, int L> __device__ __forceinline__ double g() const { return v[slot(A_, L)]; }
+  template <int J, int O> __device__ __forceinline__ double x() const { return v[S_DD + dd_index(J, O)]; }
+};
+
+// FETCH (BL): every derivative read from its work array at the point.
+struct FetchProvider {
+  const double* __restrict__ wa;
+  int64_t c, fs;
+  template <int A_, int L> __device__ __forceinline__ double g() const {
+    return __ldg(wa + slot(A_, L) * fs + c);
+  }
+  template <int J, int O> __device__ __forceinline__ double x() const {
+    return __ldg(wa + (S_DD + dd_index(J, O)) * fs + c);
+  }
+};
+
+// SS: the nine velocity gradients D(u_q, x_a) are FETCHed from work arrays
+// (ws[q*3+a]); mixed terms read the stored inner D(u_J, x_J) at outer-shifted
+// points; everything else is LOCAL (plan.py:178-179).
+template <class Acc>
+struct SSProvider {
+  const Coef& k;
+  const Acc& a;
+  const double* __restrict__ ws;
+  int64_t c, fs, st[3];
+  __device__ SSProvider(const Coef& k_, const Acc& a_, const double* ws_, int64_t c_, int64_t fs_,
+                        int64_t s0, int64_t s1)
+      : k(k_), a(a_), ws(ws_), c(c_), fs(fs_) { st[0] = s0; st[1] = s1; st[2] = 1; }
+  template <int A_, int L> __device__ __forceinline__ double g() const {
+    if constexpr (L >= S_U && L < S_U + 3) return __ldg(ws + ((L - S_U) * 3 + A_) * fs + c);
+    else return eval_slot<A_, L>(k, a);
+  }
+  template <int J, int O> __device__ __forceinline__ double x() const {
+    return d1_stored(k, O, ws + (J * 3 + J) * fs, c, st[O]);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// The five residual expressions (terms.py:151-183), left-to-right.
+// Point values: r[10] = rho, rhou0..2, rhoE, u0..2, p, T at the centre.
+// ---------------------------------------------------------------------------
+#define G(a, L) P.template g<a, L>()
+#define X(j, o) P.template x<j, o>()
+
+template <int I, class Pv>
+__device__ __forceinline__ double viscous(const Coef& k, const Pv& P) {
+  // c43*D2(u_i,x_i) + [j != i, ascending: inv_Re*D2(u_i,x_j) + c13*DD(u_j,x_i,x_j)]
+  // (terms.py:113-123)
+  constexpr int J1 = I == 0 ? 1 : 0;
+  constexpr int J2 = I == 2 ? 1 : 2;
+  return k.c43 * G(I, S_U2 + I) + k.inv_Re * G(J1, S_U2 + I) + k.c13 * X(J1, I) +
+         k.inv_Re * G(J2, S_U2 + I) + k.c13 * X(J2, I);
+}
+
+template <int I, class Pv>
+__device__ __forceinline__ double momentum(const Coef& k, const Pv& P, const double* r) {
+  const double rui = r[RU0 + I];
+  const double conv = G(0, S_RUU + I) + r[U0] * G(0, S_RU + I) + rui * G(0, S_U + 0) +
+                      G(1, S_RUU + I) + r[U1] * G(1, S_RU + I) + rui * G(1, S_U + 1) +
+                      G(2, S_RUU + I) + r[U2] * G(2, S_RU + I) + rui * G(2, S_U + 2);
+  constexpr int J1 = I == 0 ? 1 : 0;
+  constexpr int J2 = I == 2 ? 1 : 2;
+  // -(0.5*(conv)) - D(p,x_i) + viscous terms, flat chain (terms.py:164-165)
+  return -(0.5 * conv) - G(I, S_P) + k.c43 * G(I, S_U2 + I) + k.inv_Re * G(J1, S_U2 + I) +
+         k.c13 * X(J1, I) + k.inv_Re * G(J2, S_U2 + I) + k.c13 * X(J2, I);
+}
+
+template <int I, int J, class Pv>
+__device__ __forceinline__ double tau(const Coef& k, const Pv& P) {
+  // terms.py:126-132
+  if constexpr (I == J)
+    return 2.0 * k.inv_Re * G(I, S_U + I) - k.c23 * (G(0, S_U + 0) + G(1, S_U + 1) + G(2, S_U + 2));
+  else
+    return k.inv_Re * (G(J, S_U + I) + G(I, S_U + J));
+}
+
+template <class Pv>
+__device__ __forceinline__ void residual_point(const Coef& k, const Pv& P, const double* r,
+                                               double* out) {
+  // mass (terms.py:151-156)
+  {
+    const double acc = G(0, S_RU + 0) + r[U0] * G(0, S_RHO) + r[RHO] * G(0, S_U + 0) +
+                       G(1, S_RU + 1) + r[U1] * G(1, S_RHO) + r[RHO] * G(1, S_U + 1) +
+                       G(2, S_RU + 2) + r[U2] * G(2, S_RHO) + r[RHO] * G(2, S_U + 2);
+    out[0] = -(0.5 * acc);
+  }
+  out[1] = momentum<0>(k, P, r);
+  out[2] = momentum<1>(k, P, r);
+  out[3] = momentum<2>(k, P, r);
+  // energy (terms.py:167-183)
+  {
+    const double rhoe = r[RHOE_F] - 0.5 * (r[RU0] * r[U0] + r[RU1] * r[U1] + r[RU2] * r[U2]);
+    const double conv = G(0, S_RHOEU) + r[U0] * G(0, S_RHOE) + rhoe * G(0, S_U + 0) +
+                        G(1, S_RHOEU) + r[U1] * G(1, S_RHOE) + rhoe * G(1, S_U + 1) +
+                        G(2, S_RHOEU) + r[U2] * G(2, S_RHOE) + rhoe * G(2, S_U + 2);
+    const double pwork = G(0, S_UP) + G(1, S_UP) + G(2, S_UP);
+    const double heat = k.heat * (G(0, S_T2) + G(1, S_T2) + G(2, S_T2));
+    out[4] = -(0.5 * conv) - (pwork) + heat +
+             tau<0, 0>(k, P) * G(0, S_U + 0) + tau<0, 1>(k, P) * G(1, S_U + 0) +
+             tau<0, 2>(k, P) * G(2, S_U + 0) + tau<1, 0>(k, P) * G(0, S_U + 1) +
+             tau<1, 1>(k, P) * G(1, S_U + 1) + tau<1, 2>(k, P) * G(2, S_U + 1) +
+             tau<2, 0>(k, P) * G(0, S_U + 2) + tau<2, 1>(k, P) * G(1, S_U + 2) +
+             tau<2, 2>(k, P) * G(2, S_U + 2) + r[U0] * (viscous<0>(k, P)) +
+             r[U1] * (viscous<1>(k, P)) + r[U2] * (viscous<2>(k, P));
+  }
+}
+#undef G
+#undef X
+
+// Fused primitive recovery of one point (physics.py:185-202).
+__device__ __forceinline__ void primitives_point(const Coef& k, const double* q, double* prim) {
+  const double u0 = q[1] / q[0], u1 = q[2] / q[0], u2 = q[3] / q[0];
+  const double p = k.gm1 * (q[4] - 0.5 * (q[1] * u0 + q[2] * u1 + q[3] * u2));
+  prim[0] = u0; prim[1] = u1; prim[2] = u2; prim[3] = p;
+  prim[4] = k.gM2 * p / q[0];
+}
+
+}  // namespace fdns

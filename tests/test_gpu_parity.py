@@ -1,0 +1,259 @@
+"""GPU parity: every variant's CUDA path against the reference's golden
+vectors and the (reference-pinned) CPU oracle, through the C ABI.
+
+Tolerance: the north star allows rel-Linf <= 1e-12 per residual evaluation
+and 1e-10 on fields / KE / enstrophy histories over 100 steps; the kernels
+are built bitwise-faithful (-fmad=false, reference association), so the
+gates below demand EXACT equality wherever the reference is deterministic
+and apply the stated tolerances only to the device-reduced diagnostics
+(summation order differs from numpy's pairwise sum).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_linf, sha
+from oracle import c_oracle, numpy_oracle as npo
+
+pytestmark = pytest.mark.gpu
+
+fd = pytest.importorskip("paper_1610_09146_b200")
+TWO_PI = 2.0 * np.pi
+C = fd.PhysicalConstants()
+CO = npo.Consts()
+VARIANTS = fd.PLAN_NAMES
+NS_VARIANTS = ("BL", "RA", "SN", "SS")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu(built):
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def grid_of(npts):
+    return fd.make_grid(npts, (TWO_PI,) * 3)
+
+
+def state_from_cons(grid, cons):
+    from paper_1610_09146_b200.diagnostics import state_from_conservative
+    return state_from_conservative(grid, C, cons)
+
+
+def host_cons(state):
+    return state.grid.interior(state.bundle[:5]).cpu().numpy()
+
+
+def residual_of(state, variant):
+    res = fd.assemble_residual(state, C, variant)
+    torch.cuda.synchronize()
+    return res.interior_numpy()
+
+
+# ---------------------------------------------------------------- residuals
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("tag,npts", [("m16", (16, 16, 16)),
+                                      ("m_ragged", (9, 12, 7))])
+def test_residual_matches_reference_golden(golden, variant, tag, npts):
+    state = state_from_cons(grid_of(npts), golden[f"{tag}_cons"])
+    R = residual_of(state, variant)
+    ref = golden[f"{tag}_res"]
+    worst = max(rel_linf(R[q], ref[q]) for q in range(5))
+    assert worst <= 1e-12                      # north-star per-eval gate
+    assert np.array_equal(R, ref), f"{variant}/{tag}: not bitwise (rel {worst})"
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_perturbed_residual_matches_reference_golden(golden, golden_meta,
+                                                     variant):
+    F = npo.perturbed_taylor_green(16, CO, golden_meta["perturb_seed"])
+    state = state_from_cons(grid_of((16,) * 3), npo.interior(F[:5], 2))
+    assert np.array_equal(residual_of(state, variant), golden["p16_res"])
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_residual_256_matches_c_oracle(variant):
+    """Full-size single evaluation at 256^3 (C4's grid) against the C
+    oracle, bitwise."""
+    n = 256
+    F = npo.perturbed_taylor_green(n, CO, 7)
+    want = c_oracle.residual(F, CO)
+    state = state_from_cons(grid_of((n,) * 3), npo.interior(F[:5], 2))
+    got = residual_of(state, variant)
+    assert np.array_equal(got, want)
+
+
+def test_quiescent_state_zero_residual():
+    n = 8
+    shape = (n,) * 3
+    cons = np.stack([np.ones(shape), np.zeros(shape), np.zeros(shape),
+                     np.zeros(shape), np.full(shape, (1.0 / C.gM2) / C.gm1)])
+    state = state_from_cons(grid_of(shape), cons)
+    for v in VARIANTS:
+        assert np.max(np.abs(residual_of(state, v))) <= 1e-12
+
+
+# ------------------------------------------------------- primitives / halos
+def test_primitives_known_answer(golden_meta):
+    ka = golden_meta["known_answer_prim"]
+    shape = (5, 5, 5)
+    cons = np.stack([np.full(shape, 2.0), np.full(shape, 2.0),
+                     np.zeros(shape), np.zeros(shape), np.full(shape, 3.0)])
+    state = state_from_cons(grid_of(shape), cons)
+    b = state.bundle.cpu().numpy()
+    assert b[5, 3, 3, 3] == ka["u0"] == 1.0
+    assert b[8, 3, 3, 3] == ka["p"]
+    assert b[9, 3, 3, 3] == ka["T"]
+
+
+def test_primitives_bitwise_vs_oracle_over_padded():
+    F = npo.perturbed_taylor_green(12, CO, 3)
+    state = state_from_cons(grid_of((12,) * 3), npo.interior(F[:5], 2))
+    assert np.array_equal(state.to_numpy(), F)
+
+
+@pytest.mark.parametrize("npts,h", [((6, 7, 5), 2), ((8, 8, 8), 3)])
+def test_halo_wrap_matches_reference_semantics(npts, h):
+    rng = np.random.default_rng(1)
+    g = fd.make_grid(npts, (1.0, 1.0, 1.0), halo=h)
+    b = fd.mesh.alloc_bundle(g, 3)
+    host = rng.standard_normal(b.shape)
+    b.copy_(torch.from_numpy(host))
+    fd.mesh.halo_exchange_bundle(g, b, 3)
+    assert np.array_equal(b.cpu().numpy(), npo.halo_exchange(host.copy(), h))
+
+
+# ------------------------------------------------------------- time loop
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_fused_iteration_equals_unfused_substeps(variant):
+    n = 12
+    F = npo.perturbed_taylor_green(n, CO, 5)
+    g = grid_of((n,) * 3)
+    scheme = fd.RKScheme(dt=3e-3)
+    ev = fd.ResidualEvaluator(g, C, variant)
+    a = state_from_cons(g, npo.interior(F[:5], 2))
+    it = fd.IterationState(a)
+    it.save_state()
+    res = fd.Residual(g)
+    for k in range(3):
+        fd.rk_substep(it, k, scheme, ev, res)
+    b = state_from_cons(g, npo.interior(F[:5], 2))
+    fd.advance_iteration(fd.IterationState(b), scheme, ev)
+    assert np.array_equal(host_cons(a), host_cons(b))
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_c1_tgv32_10_steps_matches_reference(golden_meta, variant):
+    """Config C1 (TGV 32^3, 10 RK3 steps, dt=2e-3): final fields hash-equal
+    to the reference's."""
+    ref = golden_meta["c1_tgv32_bl"]
+    g = grid_of((32,) * 3)
+    state = fd.taylor_green_init(g, C)
+    assert [sha(f) for f in host_cons(state)] == \
+        golden_meta["tgv32_cons_sha256"]
+    ev = fd.ResidualEvaluator(g, C, variant)
+    fd.run(state, fd.RKScheme(dt=2e-3), ev, 10)
+    assert [sha(f) for f in host_cons(state)] == ref["sha256"]
+
+
+@pytest.mark.parametrize("variant", NS_VARIANTS)
+def test_c2_tgv64_100_steps(golden_meta, variant):
+    """Config C2: TGV 64^3, dt=3.385e-3, 100 RK3 steps on 1 GPU -- fields
+    bitwise equal to the reference, KE/enstrophy/conservation histories
+    within 1e-10."""
+    ref = golden_meta["c2_tgv64"]
+    g = grid_of((64,) * 3)
+    state = fd.taylor_green_init(g, C)
+    rho0 = fd.mean_density(state)
+    assert abs(rho0 - ref["rho0"]) <= 1e-13 * ref["rho0"]
+    ev = fd.ResidualEvaluator(g, C, variant)
+    rep = fd.run(state, fd.RKScheme(dt=3.385e-3), ev, 100, cadence=10,
+                 collect=fd.make_collector(g, ref["rho0"]))
+    assert [sha(f) for f in host_cons(state)] == ref["sha256"]
+    assert len(rep.records) == len(ref["history"])
+    for rec, row in zip(rep.records, ref["history"]):
+        assert rec.time == pytest.approx(row[0], rel=1e-15, abs=1e-15)
+        assert abs(rec.kinetic_energy - row[1]) <= 1e-10 * abs(row[1])
+        assert abs(rec.enstrophy - row[2]) <= 1e-10 * abs(row[2])
+        assert abs(rec.total_mass - row[3]) <= 1e-10 * abs(row[3])
+        assert abs(rec.total_energy - row[7]) <= 1e-10 * abs(row[7])
+
+
+@pytest.mark.parametrize("variant", NS_VARIANTS)
+def test_c3_perturbed_128_200_steps(golden_meta, variant):
+    """Config C3: seeded perturbed TGV 128^3, dt=1.69e-3, 200 steps."""
+    ref = golden_meta["c3_ptgv128"]
+    F = npo.perturbed_taylor_green(128, CO, golden_meta["perturb_seed"])
+    assert [sha(npo.interior(F[q], 2)) for q in range(5)] == \
+        golden_meta["c3_ptgv128_cons0_sha256"]
+    g = grid_of((128,) * 3)
+    state = state_from_cons(g, npo.interior(F[:5], 2))
+    ev = fd.ResidualEvaluator(g, C, variant)
+    rep = fd.run(state, fd.RKScheme(dt=1.69e-3), ev, 200, cadence=20,
+                 collect=fd.make_collector(g, ref["rho0"]))
+    assert [sha(f) for f in host_cons(state)] == ref["sha256"]
+    for rec, row in zip(rep.records, ref["history"]):
+        assert abs(rec.kinetic_energy - row[1]) <= 1e-10 * abs(row[1])
+        assert abs(rec.enstrophy - row[2]) <= 1e-10 * abs(row[2])
+
+
+def test_cross_variant_bitwise_after_steps():
+    n = 48
+    F = npo.perturbed_taylor_green(n, CO, 11)
+    g = grid_of((n,) * 3)
+    finals = {}
+    for v in VARIANTS:
+        s = state_from_cons(g, npo.interior(F[:5], 2))
+        fd.run(s, fd.RKScheme(dt=4e-3), fd.ResidualEvaluator(g, C, v), 5)
+        finals[v] = host_cons(s)
+    for v in VARIANTS:
+        assert np.array_equal(finals[v], finals["BL"]), v
+
+
+def test_bitwise_reproducible():
+    g = grid_of((16,) * 3)
+    runs = []
+    for _ in range(2):
+        s = fd.taylor_green_init(g, C)
+        fd.run(s, fd.RKScheme(dt=6.77e-3), fd.ResidualEvaluator(g, C, "SS"), 3)
+        runs.append(host_cons(s))
+    assert np.array_equal(*runs)
+
+
+def test_divergence_reported_with_location():
+    g = grid_of((8,) * 3)
+    s = fd.taylor_green_init(g, C)
+    with pytest.raises(fd.SolverDivergenceError) as err:
+        fd.run(s, fd.RKScheme(dt=50.0), fd.ResidualEvaluator(g, C, "SS"), 50,
+               cadence=1)
+    assert err.value.iteration is not None
+
+
+# ------------------------------------------------------------ diagnostics
+def test_tgv_initial_integrals(golden_meta):
+    g = grid_of((32,) * 3)
+    s = fd.taylor_green_init(g, C)
+    rho0 = fd.mean_density(s)
+    assert abs(rho0 - golden_meta["tgv32_rho0"]) <= 1e-14
+    ke = fd.kinetic_energy_integral(s, g, rho0)
+    en = fd.enstrophy_integral(s, g, rho0)
+    assert ke == pytest.approx(0.125, abs=1e-3)
+    assert en == pytest.approx(0.375, abs=1e-2)
+    assert abs(ke - golden_meta["tgv32_ke0"]) <= 1e-12 * golden_meta["tgv32_ke0"]
+    assert abs(en - golden_meta["tgv32_enstrophy0"]) <= \
+        1e-12 * golden_meta["tgv32_enstrophy0"]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_workarray_allocations_match_budget(variant):
+    import gc
+    g = grid_of((8,) * 3)
+    gc.collect()
+    base = fd.live_field_count()
+    ev = fd.ResidualEvaluator(g, C, variant)
+    assert fd.live_field_count() - base == fd.workarray_budget(ev.plan)
+    del ev
+    gc.collect()
+    assert fd.live_field_count() == base
