@@ -87,14 +87,18 @@ int32_t fdns_stage(int32_t variant, const double* in, const double* saved,
                    const fdns_problem* pb, void* stream);
 
 /* Device reduction of the diagnostics of a state bundle (halos current):
- * out[0] = sum 0.5*rho*|u|^2, out[1] = sum 0.5*rho*|omega|^2,
+ * out[0] = sum 0.5*rho*|u|^2, out[1] = sum 0.5*rho*|omega|^2, with rho from
+ * `state` and the velocities (fields 5-7) from `prim_state` (NULL = state;
+ * the time loop passes the bundle whose primitives the reference's
+ * ConservativeState would be holding, see timeloop.py),
  * out[2..6] = interior sums of rho, rhou0..2, rhoE, out[7] = count of
  * non-finite conservative values, out[8] = count of rho <= 0.
  * `partials` is scratch of fdns_diag_partials_size() doubles.  Replaces
  * kinetic_energy_integral / enstrophy_integral / conservation_sums /
  * check_physical (diagnostics.py:94-146, physics.py:121-129). */
 int32_t fdns_diag_partials_size(const fdns_problem* pb);
-int32_t fdns_reduce_diag(const double* state, double* partials, double* out9,
+int32_t fdns_reduce_diag(const double* state, const double* prim_state,
+                         double* partials, double* out9,
                          const fdns_problem* pb, void* stream);
 
 /* FP64 issue-rate probe: runs a DADD-only kernel for `iters` iterations and

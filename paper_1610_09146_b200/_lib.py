@@ -52,7 +52,8 @@ EXPORTS = {
     "fdns_stage": (_I, [_I, _VP, _VP, _VP, _VP, ctypes.c_double,
                         ctypes.POINTER(Problem), _VP]),
     "fdns_diag_partials_size": (_I, [ctypes.POINTER(Problem)]),
-    "fdns_reduce_diag": (_I, [_VP, _VP, _VP, ctypes.POINTER(Problem), _VP]),
+    "fdns_reduce_diag": (_I, [_VP, _VP, _VP, _VP, ctypes.POINTER(Problem),
+                              _VP]),
     "fdns_fp64_probe": (_I, [_VP, _I, _D, _VP]),
     "fdns_l2_flush": (_I, [_VP, ctypes.c_int64, _VP]),
 }

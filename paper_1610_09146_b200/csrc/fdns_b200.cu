@@ -305,6 +305,7 @@ constexpr int DIAG_THREADS = 256;
 constexpr int DIAG_BLOCKS = 148 * 4;
 
 __global__ void __launch_bounds__(DIAG_THREADS) k_diag(const double* __restrict__ in,
+                                                        const double* __restrict__ prim,
                                                         double* __restrict__ partials, Coef k,
                                                         Geom g) {
   double acc[DIAG_Q];
@@ -318,12 +319,13 @@ __global__ void __launch_bounds__(DIAG_THREADS) k_diag(const double* __restrict_
     const int ii = t / ((int64_t)g.n1 * g.n2);
     const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
     GAcc a{in, c, g.s0, g.s1, g.fs};
+    GAcc pa{prim, c, g.s0, g.s1, g.fs};   // velocities (may be another bundle)
     const double rho = a.v(RHO, 0, 0, 0);
-    const double u0 = a.v(U0, 0, 0, 0), u1 = a.v(U1, 0, 0, 0), u2 = a.v(U2, 0, 0, 0);
+    const double u0 = pa.v(U0, 0, 0, 0), u1 = pa.v(U1, 0, 0, 0), u2 = pa.v(U2, 0, 0, 0);
     acc[0] += 0.5 * rho * (u0 * u0 + u1 * u1 + u2 * u2);
-    const double w0 = d1<1, E_FIELD, U2, 0>(k, a) - d1<2, E_FIELD, U1, 0>(k, a);
-    const double w1 = d1<2, E_FIELD, U0, 0>(k, a) - d1<0, E_FIELD, U2, 0>(k, a);
-    const double w2 = d1<0, E_FIELD, U1, 0>(k, a) - d1<1, E_FIELD, U0, 0>(k, a);
+    const double w0 = d1<1, E_FIELD, U2, 0>(k, pa) - d1<2, E_FIELD, U1, 0>(k, pa);
+    const double w1 = d1<2, E_FIELD, U0, 0>(k, pa) - d1<0, E_FIELD, U2, 0>(k, pa);
+    const double w2 = d1<0, E_FIELD, U1, 0>(k, pa) - d1<1, E_FIELD, U0, 0>(k, pa);
     acc[1] += 0.5 * rho * (w0 * w0 + w1 * w1 + w2 * w2);
 #pragma unroll
     for (int f = 0; f < 5; ++f) {
@@ -524,13 +526,13 @@ int32_t fdns_stage(int32_t variant, const double* in, const double* saved, doubl
 
 int32_t fdns_diag_partials_size(const fdns_problem*) { return DIAG_BLOCKS * DIAG_Q; }
 
-int32_t fdns_reduce_diag(const double* state, double* partials, double* out9,
-                         const fdns_problem* pb, void* stream) {
+int32_t fdns_reduce_diag(const double* state, const double* prim_state, double* partials,
+                         double* out9, const fdns_problem* pb, void* stream) {
   if (int e = validate(pb)) return e;
   const Geom g = make_geom(pb);
   const Coef k = make_coef(pb);
   cudaStream_t s = (cudaStream_t)stream;
-  k_diag<<<DIAG_BLOCKS, DIAG_THREADS, 0, s>>>(state, partials, k, g);
+  k_diag<<<DIAG_BLOCKS, DIAG_THREADS, 0, s>>>(state, prim_state ? prim_state : state, partials, k, g);
   k_diag_final<<<1, 256, 0, s>>>(partials, DIAG_BLOCKS, out9);
   count(2);
   return check_launch("diagnostics kernels");

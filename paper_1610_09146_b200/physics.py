@@ -88,6 +88,9 @@ class ConservativeState:
         if bundle is None:
             bundle = alloc_bundle(grid, 10)
         self.bundle = bundle
+        # bundle whose fields 5-9 hold the primitives the reference's state
+        # would expose (None: this bundle's own); see diagnostics.reduce_state
+        self.prim_source = None
         f = [Field(grid, bundle[q]) for q in range(10)]
         self.rho, self.rhou, self.rhoE = f[0], f[1:4], f[4]
         self.u, self.p, self.T = f[5:8], f[8], f[9]
@@ -163,6 +166,7 @@ def eval_primitives_fused(state: ConservativeState,
     """u, p, T from the conservative fields over the full padded arrays
     (physics.py:185-202), one fused device pass."""
     lib = _lib.load()
+    state.prim_source = None
     _lib.check(lib.fdns_primitives(_lib.ptr(state.bundle),
                                    state.grid.problem(c),
                                    _lib.stream_handle()), "primitives")

@@ -1,0 +1,154 @@
+"""Host-side logic mirrored from the reference (CPU only): plan selector,
+storage classes, grid validation, RK scheme, stencil weights, slab
+partitioning, time-series I/O."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1610_09146_b200 as fd
+from paper_1610_09146_b200 import plan as fplan
+from oracle import numpy_oracle as npo
+
+
+def test_plan_names_and_selector():
+    assert fd.PLAN_NAMES == ("BL", "RA", "RS", "SN", "SS")   # plan.py:33
+    assert fd.build_plan("ss").name == "SS"                   # case-insensitive
+    with pytest.raises(ValueError):
+        fd.build_plan("XX")
+    assert fd.build_plan("BL").primitives == "grouped"
+    for n in ("RA", "RS", "SN", "SS"):
+        assert fd.build_plan(n).primitives == "fused"
+
+
+def test_term_list_counts():
+    ids = fplan.derivative_ids()
+    assert len(ids) == len(set(ids)) == 60                   # test_plan.py:23
+    kinds = {"d1": 0, "d2": 0, "cross": 0}
+    for d in ids:
+        kinds["cross" if d.startswith("DD") else
+              "d2" if d.startswith("D2") else "d1"] += 1
+    assert kinds == {"d1": 42, "d2": 12, "cross": 6}
+    assert set(fplan.VELOCITY_GRADIENT_IDS) <= set(ids)
+
+
+def test_storage_invariants():
+    velocity = set(fplan.VELOCITY_GRADIENT_IDS)
+    expect = {"BL": lambda d: fplan.FETCH, "RA": lambda d: fplan.INLINE,
+              "SN": lambda d: fplan.LOCAL,
+              "RS": lambda d: fplan.FETCH if d in velocity else fplan.INLINE,
+              "SS": lambda d: fplan.FETCH if d in velocity else fplan.LOCAL}
+    for name, f in expect.items():
+        for did, cls in fd.plan_storage(fd.build_plan(name)).items():
+            assert cls == f(did), (name, did)
+
+
+def test_workarray_budgets(built):
+    b = {n: fd.workarray_budget(fd.build_plan(n)) for n in fd.PLAN_NAMES}
+    # reference: BL 61 = 60 arrays + product scratch (plan.py:220-227);
+    # products are formed in registers here, so the scratch is gone
+    assert b == {"BL": 60, "RA": 0, "RS": 9, "SN": 0, "SS": 9}
+
+
+def test_grid_validation():
+    with pytest.raises(fd.ConfigurationError):
+        fd.make_grid((4, 8, 8), (1, 1, 1))
+    with pytest.raises(fd.ConfigurationError):
+        fd.make_grid((8, 8, 8), (1, -1, 1))
+    with pytest.raises(fd.ConfigurationError):
+        fd.make_grid((8, 8, 8), (1, 1, 1), halo=1)
+    with pytest.raises(fd.ConfigurationError):
+        fd.make_grid((8, 8), (1, 1))
+    g = fd.make_grid((8, 10, 12), (2 * math.pi,) * 3, halo=3)
+    assert g.shape == (14, 16, 18)
+    assert g.delta[1] == (2 * math.pi) / 10
+
+
+def test_stencil_weights_match_oracle():
+    from paper_1610_09146_b200.stencil import make_weights
+    for n in (5, 16, 64, 512):
+        d = (2 * math.pi) / n
+        w = make_weights(d)
+        assert (*w.first, *w.second) == npo.weights(d)
+
+
+def test_problem_descriptor():
+    g = fd.make_grid((16, 12, 8), (2 * math.pi,) * 3)
+    c = fd.PhysicalConstants()
+    pb = g.problem(c)
+    assert list(pb.n) == [16, 12, 8] and pb.h == 2
+    flat = [x for a in npo.grid_weights((16, 12, 8)) for x in a]
+    assert list(pb.w) == flat
+    assert list(pb.kc) == list(c.kernel_constants())
+    assert (pb.gm1, pb.gM2) == (c.gm1, c.gM2)
+
+
+def test_rk_scheme_validation():
+    s = fd.RKScheme(dt=0.1)
+    assert s.stages == 3 and s.alpha == (1.0 / 3.0, 0.5, 1.0)
+    with pytest.raises(ValueError):
+        fd.RKScheme(dt=0.0)
+    with pytest.raises(ValueError):
+        fd.RKScheme(dt=0.1, alpha=(0.5, 0.5, 0.5))
+
+
+def test_rk_stability_polynomial():
+    # save-state composition == 1 + z + z^2/2 + z^3/6 (test_timeloop.py:47-53)
+    for z in (0.05, -0.3, 0.5 + 0.2j, -1.0 + 1.0j):
+        u = 1.0
+        for a in fd.RK3_ALPHA:
+            u = 1.0 + a * z * u
+        exact = 1.0 + z + z ** 2 / 2.0 + z ** 3 / 6.0
+        assert abs(u - exact) <= 1e-13 * max(1.0, abs(exact))
+
+
+@pytest.mark.parametrize("n0,nranks", [(64, 1), (64, 2), (64, 8), (67, 3),
+                                       (1024, 8)])
+def test_slab_partition_covers_axis(n0, nranks):
+    slabs = [fd.Slab.partition(n0, r, nranks) for r in range(nranks)]
+    assert sum(s.local_n0 for s in slabs) == n0
+    assert slabs[0].offset0 == 0
+    for a, b in zip(slabs, slabs[1:]):
+        assert b.offset0 == a.offset0 + a.local_n0
+    assert max(s.local_n0 for s in slabs) - min(s.local_n0 for s in slabs) <= 1
+    assert slabs[0].down == nranks - 1 and slabs[-1].up == 0
+
+
+def test_slab_needs_halo_planes():
+    s = fd.Slab.partition(8, 0, 8)
+    with pytest.raises(fd.ConfigurationError):
+        fd.make_grid((8, 8, 8), (1, 1, 1), slab=s)
+
+
+def test_slab_grid_coordinates():
+    s = fd.Slab.partition(16, 1, 2)
+    g = fd.make_grid((16, 16, 16), (2 * math.pi,) * 3, slab=s)
+    assert g.local_npoints == (8, 16, 16)
+    assert g.shape == (12, 20, 20)
+    np.testing.assert_array_equal(g.coordinates(0),
+                                  np.arange(8, 16) * g.delta[0])
+
+
+def test_timeseries_roundtrip(tmp_path):
+    recs = [fd.DiagnosticsRecord(0.1 * i, 0.125 + i * 1e-17, 0.375, 1.0,
+                                 (0.0, 1e-300, -2.5), 178.6) for i in range(3)]
+    p = tmp_path / "ts.csv"
+    fd.write_timeseries(recs, p)
+    assert p.read_text().splitlines()[0] == \
+        "time,ke,enstrophy,mass,mom0,mom1,mom2,energy"
+    assert fd.read_timeseries(p) == recs
+    p.write_text("bad,header\n")
+    with pytest.raises(ValueError):
+        fd.read_timeseries(p)
+
+
+def test_no_cpu_fallback_without_gpu(built):
+    """The product path fails loudly when no CUDA device is present."""
+    import torch
+    from paper_1610_09146_b200 import _lib
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    g = fd.make_grid((8, 8, 8), (2 * math.pi,) * 3)
+    with pytest.raises(_lib.FdnsError):
+        fd.taylor_green_init(g, fd.PhysicalConstants())
