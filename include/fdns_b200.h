@@ -78,13 +78,20 @@ int32_t fdns_rk_update(double* cons, const double* saved, const double* res,
 
 /* One fused RK stage: residual of `in` (a state bundle with current halos)
  * under the variant, q = saved + coef*R, primitives of q, all written to the
- * interior of the `out` state bundle (halos are left to fdns_halo_wrap / the
- * slab exchange).  `saved` is 5 conservative fields and may alias `out`
- * (pointwise update).  Bitwise equal to fdns_residual + fdns_rk_update +
- * fdns_primitives -- replaces rk_substep (timeloop.py:75-85). */
+ * interior of the `out` state bundle AND to each point's periodic ghost
+ * images on the axes in wrap_mask (0b111 on one GPU; 0b110 for a z-slab
+ * rank, whose axis-0 ghosts come from the slab exchange).  `saved` is 5
+ * conservative fields and may alias `out` (pointwise update).  Bitwise equal
+ * to fdns_residual + fdns_rk_update + fdns_halo_wrap + fdns_primitives --
+ * replaces rk_substep (timeloop.py:75-85). */
 int32_t fdns_stage(int32_t variant, const double* in, const double* saved,
-                   double* out, double* work, double coef,
+                   double* out, double* work, double coef, int32_t wrap_mask,
                    const fdns_problem* pb, void* stream);
+
+/* Test hook: 1 = run every variant on the one-thread-per-point kernels
+ * (global-memory taps), 0 = default (TMA-staged tiled kernels where the
+ * row pitch allows).  Both paths are parity-tested. */
+void fdns_set_kernel_path(int32_t point_only);
 
 /* Device reduction of the diagnostics of a state bundle (halos current):
  * out[0] = sum 0.5*rho*|u|^2, out[1] = sum 0.5*rho*|omega|^2, with rho from

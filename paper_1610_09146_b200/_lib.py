@@ -49,8 +49,9 @@ EXPORTS = {
     "fdns_residual": (_I, [_I, _VP, _VP, _VP, ctypes.POINTER(Problem), _VP]),
     "fdns_rk_update": (_I, [_VP, _VP, _VP, ctypes.c_double,
                             ctypes.POINTER(Problem), _VP]),
-    "fdns_stage": (_I, [_I, _VP, _VP, _VP, _VP, ctypes.c_double,
+    "fdns_stage": (_I, [_I, _VP, _VP, _VP, _VP, ctypes.c_double, _I,
                         ctypes.POINTER(Problem), _VP]),
+    "fdns_set_kernel_path": (None, [_I]),
     "fdns_diag_partials_size": (_I, [ctypes.POINTER(Problem)]),
     "fdns_reduce_diag": (_I, [_VP, _VP, _VP, _VP, ctypes.POINTER(Problem),
                               _VP]),

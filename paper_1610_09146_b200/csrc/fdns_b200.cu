@@ -12,6 +12,9 @@
 
 #include "../../include/fdns_b200.h"
 #include "fdns_math.cuh"
+#include "fdns_tiled.cuh"
+
+#include <cudaTypedefs.h>
 
 
 using namespace fdns;
@@ -19,6 +22,7 @@ using namespace fdns;
 namespace {
 
 thread_local std::string g_err;
+bool g_force_point = false;   // test hook: run the point kernels everywhere
 std::atomic<long long> g_launches{0};
 inline void count(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
@@ -153,7 +157,7 @@ template <int V, int MODE>
 __global__ void __launch_bounds__(256) k_residual(const double* __restrict__ in,
                                                   const double* saved, double* out,
                                                   const double* __restrict__ work, Coef k,
-                                                  Geom g, double coef) {
+                                                  Geom g, double coef, int wrap_mask) {
   const int kk = blockIdx.x * blockDim.x + threadIdx.x;
   const int jj = blockIdx.y * blockDim.y + threadIdx.y;
   const int ii = blockIdx.z;
@@ -184,17 +188,13 @@ __global__ void __launch_bounds__(256) k_residual(const double* __restrict__ in,
     residual_point(k, P, r, R);
   }
   if constexpr (MODE == 0) {
-#pragma unroll
-    for (int f = 0; f < 5; ++f) out[f * g.fs + c] = R[f];
+    tiled::emit<5>(out, g, ii, jj, kk, R, 0);
   } else {
-    double q[5], pr[5];
+    double q[NFIELDS];
 #pragma unroll
     for (int f = 0; f < 5; ++f) q[f] = saved[f * g.fs + c] + coef * R[f];
-    primitives_point(k, q, pr);
-#pragma unroll
-    for (int f = 0; f < 5; ++f) out[f * g.fs + c] = q[f];
-#pragma unroll
-    for (int f = 0; f < 5; ++f) out[(5 + f) * g.fs + c] = pr[f];
+    primitives_point(k, q, q + 5);
+    tiled::emit<NFIELDS>(out, g, ii, jj, kk, q, wrap_mask);
   }
 }
 
@@ -390,17 +390,111 @@ inline dim3 point_grid(const Geom& g, dim3 blk) {
   return dim3((g.n2 + blk.x - 1) / blk.x, (g.n1 + blk.y - 1) / blk.y, g.n0);
 }
 
+// ---------------------------------------------------------------------------
+// TMA tensor map of a state bundle viewed as 4-D (k, j, i, field), box = one
+// staged plane (TK+4, TJ+4, 1, 10).  Needs an even padded row (16-byte row
+// pitch); otherwise the point kernels run.
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool plane_map(CUtensorMap* m, const double* base, const Geom& g) {
+  const int64_t P2 = g.n2 + 2 * g.h, P1 = g.n1 + 2 * g.h, P0 = g.n0 + 2 * g.h;
+  if (P2 % 2 != 0) return false;
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0) return false;
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)P2, (cuuint64_t)P1, (cuuint64_t)P0, (cuuint64_t)NFIELDS};
+  cuuint64_t strides[3] = {(cuuint64_t)(P2 * 8), (cuuint64_t)(P1 * P2 * 8),
+                           (cuuint64_t)(g.fs * 8)};
+  cuuint32_t box[4] = {tiled::PK, tiled::PJ, 1, NFIELDS};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Planes per CTA along axis 0: minimise waves x (planes + ramp) for one CTA
+// per SM.
+int pick_chunk(const Geom& g, int num_sms) {
+  const int64_t tiles = (int64_t)((g.n2 + tiled::TK - 1) / tiled::TK) *
+                        ((g.n1 + tiled::TJ - 1) / tiled::TJ);
+  int best = g.n0;
+  double best_cost = 1e300;
+  for (int c = 4; c <= g.n0; ++c) {
+    const int64_t nchunks = (g.n0 + c - 1) / c;
+    const int64_t waves = (tiles * nchunks + num_sms - 1) / num_sms;
+    const double cost = waves * (c + 1.5);
+    if (cost < best_cost - 1e-9) { best_cost = cost; best = c; }
+  }
+  return std::max(1, std::min(best, g.n0));
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <int V, int MODE>
+int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const double* work,
+                   const Coef& k, const Geom& g, double coef, int wrap, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tiled::k_stage_tiled<V, MODE>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, tiled::SMEM_BYTES);
+    attr = true;
+  }
+  const int chunk = pick_chunk(g, num_sms());
+  const dim3 grd((g.n2 + tiled::TK - 1) / tiled::TK, (g.n1 + tiled::TJ - 1) / tiled::TJ,
+                 (g.n0 + chunk - 1) / chunk);
+  tiled::k_stage_tiled<V, MODE><<<grd, tiled::NT, tiled::SMEM_BYTES, s>>>(
+      m, work, saved, out, k, g, coef, chunk, wrap);
+  return 0;
+}
+
 template <int MODE>
 int launch_residual(int variant, const double* in, const double* saved, double* out,
-                    double* work, const Coef& k, const Geom& g, double coef, cudaStream_t s) {
+                    double* work, const Coef& k, const Geom& g, double coef, int wrap,
+                    cudaStream_t s) {
+  CUtensorMap m;
+  if (variant != FDNS_BL && !g_force_point && plane_map(&m, in, g)) {
+    switch (variant) {
+      case FDNS_RA: launch_tiled_v<FDNS_RA, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
+      case FDNS_RS: launch_tiled_v<FDNS_RS, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
+      case FDNS_SN: launch_tiled_v<FDNS_SN, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
+      case FDNS_SS: launch_tiled_v<FDNS_SS, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
+      default: return fail("unknown variant");
+    }
+    count();
+    return check_launch("tiled stage kernel");
+  }
   const dim3 blk(32, 8, 1);
   const dim3 grd = point_grid(g, blk);
   switch (variant) {
-    case FDNS_BL: k_residual<FDNS_BL, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef); break;
-    case FDNS_RA: k_residual<FDNS_RA, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef); break;
-    case FDNS_RS: k_residual<FDNS_RS, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef); break;
-    case FDNS_SN: k_residual<FDNS_SN, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef); break;
-    case FDNS_SS: k_residual<FDNS_SS, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef); break;
+    case FDNS_BL: k_residual<FDNS_BL, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap); break;
+    case FDNS_RA: k_residual<FDNS_RA, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap); break;
+    case FDNS_RS: k_residual<FDNS_RS, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap); break;
+    case FDNS_SN: k_residual<FDNS_SN, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap); break;
+    case FDNS_SS: k_residual<FDNS_SS, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap); break;
     default: return fail("unknown variant");
   }
   count();
@@ -446,6 +540,8 @@ const char* fdns_last_error(void) { return g_err.c_str(); }
 int32_t fdns_abi_version(void) { return 1; }
 
 int64_t fdns_launch_count(void) { return g_launches.load(); }
+
+void fdns_set_kernel_path(int32_t point_only) { g_force_point = point_only != 0; }
 
 int32_t fdns_workarray_count(int32_t variant) {
   switch (variant) {
@@ -497,7 +593,7 @@ int32_t fdns_residual(int32_t variant, const double* state, double* work, double
   const Coef k = make_coef(pb);
   cudaStream_t s = (cudaStream_t)stream;
   if (int e = launch_fills(variant, state, work, k, g, s)) return e;
-  return launch_residual<0>(variant, state, nullptr, out, work, k, g, 0.0, s);
+  return launch_residual<0>(variant, state, nullptr, out, work, k, g, 0.0, 0, s);
 }
 
 int32_t fdns_rk_update(double* cons, const double* saved, const double* res, double coef,
@@ -511,7 +607,8 @@ int32_t fdns_rk_update(double* cons, const double* saved, const double* res, dou
 }
 
 int32_t fdns_stage(int32_t variant, const double* in, const double* saved, double* out,
-                   double* work, double coef, const fdns_problem* pb, void* stream) {
+                   double* work, double coef, int32_t wrap_mask, const fdns_problem* pb,
+                   void* stream) {
   if (int e = validate(pb)) return e;
   const int nw = fdns_workarray_count(variant);
   if (nw < 0) return fail("unknown variant");
@@ -521,7 +618,7 @@ int32_t fdns_stage(int32_t variant, const double* in, const double* saved, doubl
   const Coef k = make_coef(pb);
   cudaStream_t s = (cudaStream_t)stream;
   if (int e = launch_fills(variant, in, work, k, g, s)) return e;
-  return launch_residual<1>(variant, in, saved, out, work, k, g, coef, s);
+  return launch_residual<1>(variant, in, saved, out, work, k, g, coef, wrap_mask, s);
 }
 
 int32_t fdns_diag_partials_size(const fdns_problem*) { return DIAG_BLOCKS * DIAG_Q; }

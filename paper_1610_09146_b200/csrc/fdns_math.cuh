@@ -43,6 +43,7 @@ struct Geom {
 // Global-memory accessor through the read-only path.  Loads may be merged by
 // the compiler (used by LOCAL/FETCH providers).
 struct GAcc {
+  static constexpr bool kInternalEnergy = false;
   const double* __restrict__ b;
   int64_t c, s0, s1, fs;
   __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
@@ -54,6 +55,7 @@ struct GAcc {
 // neither the loads nor the arithmetic built on them: every occurrence of a
 // derivative is genuinely recomputed (RA semantics, plan.py:172-173).
 struct VAcc {
+  static constexpr bool kInternalEnergy = false;
   const double* b;
   int64_t c, s0, s1, fs;
   __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
@@ -73,12 +75,20 @@ template <int AX> struct Off {
   }
 };
 
+// Internal energy rho*e at a point (terms.py:39).  Accessors over staged
+// tiles hold it precomputed in place of rhoE (kInternalEnergy): the same
+// per-point expression, evaluated once per staged point instead of once per
+// stencil tap, so the bits are identical.
 template <class A>
 __device__ __forceinline__ double rhoe_at(const A& a, int di, int dj, int dk) {
-  return a.v(RHOE_F, di, dj, dk) -
-         0.5 * (a.v(RU0, di, dj, dk) * a.v(U0, di, dj, dk) +
-                a.v(RU1, di, dj, dk) * a.v(U1, di, dj, dk) +
-                a.v(RU2, di, dj, dk) * a.v(U2, di, dj, dk));
+  if constexpr (A::kInternalEnergy) {
+    return a.v(RHOE_F, di, dj, dk);
+  } else {
+    return a.v(RHOE_F, di, dj, dk) -
+           0.5 * (a.v(RU0, di, dj, dk) * a.v(U0, di, dj, dk) +
+                  a.v(RU1, di, dj, dk) * a.v(U1, di, dj, dk) +
+                  a.v(RU2, di, dj, dk) * a.v(U2, di, dj, dk));
+  }
 }
 
 // Expression kinds differentiated by the stencils.
@@ -282,7 +292,8 @@ __device__ __forceinline__ double tau(const Coef& k, const Pv& P) {
     return k.inv_Re * (G(J, S_U + I) + G(I, S_U + J));
 }
 
-template <class Pv>
+// RHOE_INTERNAL: r[RHOE_F] already holds rho*e (staged-tile accessors).
+template <bool RHOE_INTERNAL = false, class Pv>
 __device__ __forceinline__ void residual_point(const Coef& k, const Pv& P, const double* r,
                                                double* out) {
   // mass (terms.py:151-156)
@@ -297,7 +308,9 @@ __device__ __forceinline__ void residual_point(const Coef& k, const Pv& P, const
   out[3] = momentum<2>(k, P, r);
   // energy (terms.py:167-183)
   {
-    const double rhoe = r[RHOE_F] - 0.5 * (r[RU0] * r[U0] + r[RU1] * r[U1] + r[RU2] * r[U2]);
+    const double rhoe = RHOE_INTERNAL ? r[RHOE_F]
+                                      : r[RHOE_F] - 0.5 * (r[RU0] * r[U0] + r[RU1] * r[U1] +
+                                                           r[RU2] * r[U2]);
     const double conv = G(0, S_RHOEU) + r[U0] * G(0, S_RHOE) + rhoe * G(0, S_U + 0) +
                         G(1, S_RHOEU) + r[U1] * G(1, S_RHOE) + rhoe * G(1, S_U + 1) +
                         G(2, S_RHOEU) + r[U2] * G(2, S_RHOE) + rhoe * G(2, S_U + 2);

@@ -149,12 +149,20 @@ class ResidualEvaluator:
                                alloc_bundle(self.grid, 10))
         return self._workspace
 
+    @property
+    def wrap_mask(self) -> int:
+        """Axes whose ghosts the stage kernel fills in place (all three on
+        one GPU; axis 0 comes from the slab exchange on several)."""
+        slab = self.grid.slab
+        return 0b110 if slab is not None and slab.nranks > 1 else 0b111
+
     def stage(self, inp: torch.Tensor, saved: torch.Tensor, out: torch.Tensor,
               coef: float) -> None:
-        """One fused RK stage (residual + update + primitives) into `out`."""
+        """One fused RK stage (residual + update + primitives + periodic
+        ghost images) into `out`."""
         _lib.check(self.lib.fdns_stage(
             self.plan.variant_id, _lib.ptr(inp), _lib.ptr(saved),
-            _lib.ptr(out), self.work_ptr, coef, self.problem,
+            _lib.ptr(out), self.work_ptr, coef, self.wrap_mask, self.problem,
             _lib.stream_handle()), f"stage ({self.plan.name})")
 
 
