@@ -172,8 +172,8 @@ __global__ void __launch_bounds__(256) k_residual(const double* __restrict__ in,
     LocalProvider<GAcc> P(k, a);
     residual_point(k, P, r, R);
   } else if constexpr (V == FDNS_RA) {
-    VAcc a{in, c, g.s0, g.s1, g.fs};
-    InlineProvider<VAcc> P(k, a);
+    GAcc a{in, c, g.s0, g.s1, g.fs};
+    InlineProvider<GAcc> P(k, a);
     residual_point(k, P, r, R);
   } else if constexpr (V == FDNS_BL) {
     FetchProvider P{work, c, g.fs};
@@ -183,8 +183,8 @@ __global__ void __launch_bounds__(256) k_residual(const double* __restrict__ in,
     SSProvider<GAcc> P(k, a, work, c, g.fs, g.s0, g.s1);
     residual_point(k, P, r, R);
   } else {  // RS: stored velocity gradients, everything else inline
-    VAcc a{in, c, g.s0, g.s1, g.fs};
-    SSProvider<VAcc> P(k, a, work, c, g.fs, g.s0, g.s1);
+    GAcc a{in, c, g.s0, g.s1, g.fs};
+    SSProvider<GAcc, true> P(k, a, work, c, g.fs, g.s0, g.s1);
     residual_point(k, P, r, R);
   }
   if constexpr (MODE == 0) {
@@ -427,22 +427,6 @@ bool plane_map(CUtensorMap* m, const double* base, const Geom& g) {
   return r == CUDA_SUCCESS;
 }
 
-// Planes per CTA along axis 0: minimise waves x (planes + ramp) for one CTA
-// per SM.
-int pick_chunk(const Geom& g, int num_sms) {
-  const int64_t tiles = (int64_t)((g.n2 + tiled::TK - 1) / tiled::TK) *
-                        ((g.n1 + tiled::TJ - 1) / tiled::TJ);
-  int best = g.n0;
-  double best_cost = 1e300;
-  for (int c = 4; c <= g.n0; ++c) {
-    const int64_t nchunks = (g.n0 + c - 1) / c;
-    const int64_t waves = (tiles * nchunks + num_sms - 1) / num_sms;
-    const double cost = waves * (c + 1.5);
-    if (cost < best_cost - 1e-9) { best_cost = cost; best = c; }
-  }
-  return std::max(1, std::min(best, g.n0));
-}
-
 int g_num_sms = 0;
 int num_sms() {
   if (!g_num_sms) {
@@ -457,17 +441,20 @@ int num_sms() {
 template <int V, int MODE>
 int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const double* work,
                    const Coef& k, const Geom& g, double coef, int wrap, cudaStream_t s) {
+  constexpr int smem = V == FDNS_SN ? tiled::SMEM_BYTES_SN : tiled::SMEM_BYTES;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tiled::k_stage_tiled<V, MODE>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, tiled::SMEM_BYTES);
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  const int chunk = pick_chunk(g, num_sms());
-  const dim3 grd((g.n2 + tiled::TK - 1) / tiled::TK, (g.n1 + tiled::TJ - 1) / tiled::TJ,
-                 (g.n0 + chunk - 1) / chunk);
-  tiled::k_stage_tiled<V, MODE><<<grd, tiled::NT, tiled::SMEM_BYTES, s>>>(
-      m, work, saved, out, k, g, coef, chunk, wrap);
+  const int ntk = (g.n2 + tiled::TK - 1) / tiled::TK;
+  const int ntj = (g.n1 + tiled::TJ - 1) / tiled::TJ;
+  const int64_t total = (int64_t)ntk * ntj * g.n0;
+  // one persistent CTA per SM, each at least ~4 plane steps
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(num_sms(), total / 4));
+  tiled::k_stage_tiled<V, MODE><<<(unsigned)ctas, tiled::NT, smem, s>>>(
+      m, work, saved, out, k, g, coef, ntk, total, wrap);
   return 0;
 }
 

@@ -49,22 +49,23 @@ struct GAcc {
   __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
     return __ldg(b + f * fs + c + di * s0 + dj * s1 + dk);
   }
+  __device__ __forceinline__ GAcc rebased(int z) const { return GAcc{b, c + z, s0, s1, fs}; }
 };
 
-// Global-memory accessor whose loads are volatile, so the compiler can merge
-// neither the loads nor the arithmetic built on them: every occurrence of a
-// derivative is genuinely recomputed (RA semantics, plan.py:172-173).
-struct VAcc {
-  static constexpr bool kInternalEnergy = false;
-  const double* b;
-  int64_t c, s0, s1, fs;
-  __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
-    const double* p = b + f * fs + c + di * s0 + dj * s1 + dk;
-    double r;
-    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
-    return r;
-  }
-};
+// Occurrence-distinct zero offsets (RA semantics, plan.py:172-173).  The
+// INLINE provider rebases every derivative occurrence's tap addresses by
+// g_zero_offset[occurrence]: all entries are 0 at run time, but the compiler
+// cannot prove two entries equal, so it can merge neither the loads nor the
+// arithmetic built on them -- each occurrence is genuinely recomputed, as
+// in the reference's generated RA kernel.  Integer offsets keep the bits
+// exact (a floating-point +0.0 would not: it flips -0.0).
+constexpr int N_ZERO_OFFSETS = 4096;
+__constant__ int g_zero_offset[N_ZERO_OFFSETS];
+
+template <int OCC>
+__device__ __forceinline__ int zero_offset() {
+  return g_zero_offset[OCC % N_ZERO_OFFSETS];
+}
 
 // ---------------------------------------------------------------------------
 // Point expressions of the term list (terms.py:39, :158-174)
@@ -187,14 +188,18 @@ __device__ __forceinline__ double eval_slot(const Coef& k, const Acc& a) {
 // Providers
 // ---------------------------------------------------------------------------
 
-// INLINE (RA): every call re-expands the stencil.
+// INLINE (RA): every occurrence re-expands the stencil from rebased taps.
 template <class Acc>
 struct InlineProvider {
   const Coef& k;
   const Acc& a;
   __device__ InlineProvider(const Coef& k_, const Acc& a_) : k(k_), a(a_) {}
-  template <int A_, int L> __device__ __forceinline__ double g() const { return eval_slot<A_, L>(k, a); }
-  template <int J, int O> __device__ __forceinline__ double x() const { return dd<O, J>(k, a); }
+  template <int A_, int L, int OCC = 0> __device__ __forceinline__ double g() const {
+    return eval_slot<A_, L>(k, a.rebased(zero_offset<OCC>()));
+  }
+  template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const {
+    return dd<O, J>(k, a.rebased(zero_offset<OCC>()));
+  }
 };
 
 // LOCAL (SN): each distinct derivative evaluated once into a local.
@@ -216,26 +221,27 @@ struct LocalProvider {
     v[S_DD + dd_index(0, 2)] = dd<2, 0>(k, a);
     v[S_DD + dd_index(1, 2)] = dd<2, 1>(k, a);
   }
-  template <int A_, int L> __device__ __forceinline__ double g() const { return v[slot(A_, L)]; }
-  template <int J, int O> __device__ __forceinline__ double x() const { return v[S_DD + dd_index(J, O)]; }
+  template <int A_, int L, int OCC = 0> __device__ __forceinline__ double g() const { return v[slot(A_, L)]; }
+  template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const { return v[S_DD + dd_index(J, O)]; }
 };
 
 // FETCH (BL): every derivative read from its work array at the point.
 struct FetchProvider {
   const double* __restrict__ wa;
   int64_t c, fs;
-  template <int A_, int L> __device__ __forceinline__ double g() const {
+  template <int A_, int L, int OCC = 0> __device__ __forceinline__ double g() const {
     return __ldg(wa + slot(A_, L) * fs + c);
   }
-  template <int J, int O> __device__ __forceinline__ double x() const {
+  template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const {
     return __ldg(wa + (S_DD + dd_index(J, O)) * fs + c);
   }
 };
 
-// SS: the nine velocity gradients D(u_q, x_a) are FETCHed from work arrays
-// (ws[q*3+a]); mixed terms read the stored inner D(u_J, x_J) at outer-shifted
-// points; everything else is LOCAL (plan.py:178-179).
-template <class Acc>
+// SS / RS: the nine velocity gradients D(u_q, x_a) are FETCHed from work
+// arrays (ws[q*3+a]); mixed terms read the stored inner D(u_J, x_J) at
+// outer-shifted points; everything else is LOCAL (SS, plan.py:178-179) or
+// re-expanded at every occurrence (RS, INLINE, plan.py:176-177).
+template <class Acc, bool INLINE_REST = false>
 struct SSProvider {
   const Coef& k;
   const Acc& a;
@@ -244,11 +250,12 @@ struct SSProvider {
   __device__ SSProvider(const Coef& k_, const Acc& a_, const double* ws_, int64_t c_, int64_t fs_,
                         int64_t s0, int64_t s1)
       : k(k_), a(a_), ws(ws_), c(c_), fs(fs_) { st[0] = s0; st[1] = s1; st[2] = 1; }
-  template <int A_, int L> __device__ __forceinline__ double g() const {
+  template <int A_, int L, int OCC = 0> __device__ __forceinline__ double g() const {
     if constexpr (L >= S_U && L < S_U + 3) return __ldg(ws + ((L - S_U) * 3 + A_) * fs + c);
+    else if constexpr (INLINE_REST) return eval_slot<A_, L>(k, a.rebased(zero_offset<OCC>()));
     else return eval_slot<A_, L>(k, a);
   }
-  template <int J, int O> __device__ __forceinline__ double x() const {
+  template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const {
     return d1_stored(k, O, ws + (J * 3 + J) * fs, c, st[O]);
   }
 };
@@ -257,11 +264,16 @@ struct SSProvider {
 // The five residual expressions (terms.py:151-183), left-to-right.
 // Point values: r[10] = rho, rhou0..2, rhoE, u0..2, p, T at the centre.
 // ---------------------------------------------------------------------------
-#define G(a, L) P.template g<a, L>()
-#define X(j, o) P.template x<j, o>()
+// Each G/X call site gets a distinct occurrence id (__COUNTER__), salted by
+// the helper's template arguments so that e.g. the three div(u) sums inside
+// tau<0,0>, tau<1,1>, tau<2,2> stay distinct occurrences, as in the
+// reference's expression strings.
+#define G(a, L) P.template g<a, L, __COUNTER__ * 16 + SALT>()
+#define X(j, o) P.template x<j, o, __COUNTER__ * 16 + SALT>()
 
 template <int I, class Pv>
 __device__ __forceinline__ double viscous(const Coef& k, const Pv& P) {
+  constexpr int SALT = 1 + I;
   // c43*D2(u_i,x_i) + [j != i, ascending: inv_Re*D2(u_i,x_j) + c13*DD(u_j,x_i,x_j)]
   // (terms.py:113-123)
   constexpr int J1 = I == 0 ? 1 : 0;
@@ -272,6 +284,7 @@ __device__ __forceinline__ double viscous(const Coef& k, const Pv& P) {
 
 template <int I, class Pv>
 __device__ __forceinline__ double momentum(const Coef& k, const Pv& P, const double* r) {
+  constexpr int SALT = 4 + I;
   const double rui = r[RU0 + I];
   const double conv = G(0, S_RUU + I) + r[U0] * G(0, S_RU + I) + rui * G(0, S_U + 0) +
                       G(1, S_RUU + I) + r[U1] * G(1, S_RU + I) + rui * G(1, S_U + 1) +
@@ -285,6 +298,7 @@ __device__ __forceinline__ double momentum(const Coef& k, const Pv& P, const dou
 
 template <int I, int J, class Pv>
 __device__ __forceinline__ double tau(const Coef& k, const Pv& P) {
+  constexpr int SALT = 7 + I * 3 + J - (I * 3 + J > 8 ? 9 : 0);
   // terms.py:126-132
   if constexpr (I == J)
     return 2.0 * k.inv_Re * G(I, S_U + I) - k.c23 * (G(0, S_U + 0) + G(1, S_U + 1) + G(2, S_U + 2));
@@ -296,6 +310,7 @@ __device__ __forceinline__ double tau(const Coef& k, const Pv& P) {
 template <bool RHOE_INTERNAL = false, class Pv>
 __device__ __forceinline__ void residual_point(const Coef& k, const Pv& P, const double* r,
                                                double* out) {
+  constexpr int SALT = 0;
   // mass (terms.py:151-156)
   {
     const double acc = G(0, S_RU + 0) + r[U0] * G(0, S_RHO) + r[RHO] * G(0, S_U + 0) +

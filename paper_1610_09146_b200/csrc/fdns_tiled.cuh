@@ -77,6 +77,12 @@ struct SAcc {
   __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
     return p[di + 2][f * PLANE + dj * PK + dk];
   }
+  __device__ __forceinline__ SAcc rebased(int z) const {
+    SAcc r;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) r.p[d] = p[d] + z;
+    return r;
+  }
 };
 
 // Write the 10 (MODE 1) or 5 (MODE 0) output values of interior point
@@ -129,21 +135,75 @@ __device__ __forceinline__ void to_internal_energy(double* slot) {
   }
 }
 
+// Centre-plane inner-derivative buffers (SN): D(u0,x0), D(u1,x1), D(u2,x2)
+// over the staged box, so the in-plane mixed terms read 4 values each
+// instead of re-expanding 4 inner stencils (same stencil shape at every
+// point: bitwise equal to the reference's re-expansion, codegen.py:97-102).
+constexpr int NBUF = 3;
+constexpr int SMEM_BYTES_SN = NR * SLOT * 8 + NBUF * PLANE * 8 + 128;
+
+// SN provider over the staged tile: every distinct derivative once (LOCAL),
+// diagonal velocity gradients and the six mixed terms from the axis-0
+// register queues (q1, q2: D(u1,x1), D(u2,x2) at this column on planes
+// i-2..i+2) and the centre-plane buffers.
+struct TiledLocalProvider {
+  double v[N_SLOTS];
+  template <int A_, int L>
+  __device__ __forceinline__ void fill1(const Coef& k, const SAcc& a) {
+    if constexpr (!(L >= S_U && L < S_U + 3 && (L - S_U) == A_)) v[slot(A_, L)] = eval_slot<A_, L>(k, a);
+    if constexpr (L + 1 < S_PER_AXIS) fill1<A_, L + 1>(k, a);
+  }
+  __device__ __forceinline__ TiledLocalProvider(const Coef& k, const SAcc& a, const double* q1,
+                                                const double* q2, const double* bu0,
+                                                const double* bu1, const double* bu2) {
+    fill1<0, 0>(k, a);
+    fill1<1, 0>(k, a);
+    fill1<2, 0>(k, a);
+    v[slot(0, S_U + 0)] = bu0[0];
+    v[slot(1, S_U + 1)] = q1[2];
+    v[slot(2, S_U + 2)] = q2[2];
+    // DD(u1,x0,x1), DD(u2,x0,x2): outer axis 0 over the queues
+    v[S_DD + dd_index(1, 0)] = k.w1[0] * (q1[3] - q1[1]) + k.w2[0] * (q1[4] - q1[0]);
+    v[S_DD + dd_index(2, 0)] = k.w1[0] * (q2[3] - q2[1]) + k.w2[0] * (q2[4] - q2[0]);
+    // DD(u0,x1,x0), DD(u0,x2,x0): outer axes 1, 2 over D(u0,x0)
+    v[S_DD + dd_index(0, 1)] = k.w1[1] * (bu0[PK] - bu0[-PK]) + k.w2[1] * (bu0[2 * PK] - bu0[-2 * PK]);
+    v[S_DD + dd_index(0, 2)] = k.w1[2] * (bu0[1] - bu0[-1]) + k.w2[2] * (bu0[2] - bu0[-2]);
+    // DD(u2,x1,x2): outer axis 1 over D(u2,x2); DD(u1,x2,x1): outer axis 2 over D(u1,x1)
+    v[S_DD + dd_index(2, 1)] = k.w1[1] * (bu2[PK] - bu2[-PK]) + k.w2[1] * (bu2[2 * PK] - bu2[-2 * PK]);
+    v[S_DD + dd_index(1, 2)] = k.w1[2] * (bu1[1] - bu1[-1]) + k.w2[2] * (bu1[2] - bu1[-2]);
+  }
+  template <int A_, int L, int OCC = 0> __device__ __forceinline__ double g() const { return v[slot(A_, L)]; }
+  template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const { return v[S_DD + dd_index(J, O)]; }
+};
+
+// Static, balanced work split of one stage: the (tile, plane) steps in
+// tile-major order are cut into gridDim.x equal ranges; a CTA walks its
+// range as <= a few segments (one per tile touched).  The TMA producer
+// (thread 0) streams the planes of all segments back to back through the
+// ring, prefetching across segment boundaries.
+struct Segments {
+  int64_t beg, end;   // [beg, end) in tile-major (tile * n0 + plane) order
+  int n0;
+  __device__ __forceinline__ int64_t seg_end(int64_t x) const {
+    const int64_t tile_end = (x / n0 + 1) * (int64_t)n0;
+    return tile_end < end ? tile_end : end;
+  }
+};
+
 template <int V, int MODE>
 __global__ void __launch_bounds__(NT, 1)
     k_stage_tiled(const __grid_constant__ CUtensorMap tin, const double* __restrict__ work,
-                  const double* saved, double* out, Coef k, Geom g, double coef, int chunk,
-                  int wrap_mask) {
+                  const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
+                  int64_t total_steps, int wrap_mask) {
   extern __shared__ __align__(128) double sm[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NR * SLOT);
+  constexpr bool kBuf = (V == FDNS_SN);
+  double* bufs = sm + NR * SLOT;   // NBUF planes (SN only)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NR * SLOT + (kBuf ? NBUF * PLANE : 0));
   const int tid = threadIdx.x;
   const int tk = tid % TK, tj = tid / TK;
-  const int k0 = blockIdx.x * TK, j0 = blockIdx.y * TJ;
-  const int i0 = blockIdx.z * chunk;
-  const int i1 = min(i0 + chunk, g.n0);
-  if (i0 >= i1) return;
-  const int nsteps = i1 - i0;
-  const int nseq = nsteps + 4;   // planes i0-2 .. i1+1
+  Segments S{blockIdx.x * total_steps / gridDim.x, (blockIdx.x + 1) * total_steps / gridDim.x,
+             g.n0};
+  if (S.beg >= S.end) return;
 
   if (tid == 0) {
 #pragma unroll
@@ -152,70 +212,121 @@ __global__ void __launch_bounds__(NT, 1)
   }
   __syncthreads();
 
-  auto issue = [&](int s) {
-    const int slot = s % NR;
+  // producer cursor (thread 0): stream position, current segment, position
+  // within it
+  int64_t p_seg = S.beg;
+  int p_r = 0;
+  int issued = 0;
+  auto issue_next = [&]() {
+    const int64_t se = S.seg_end(p_seg);
+    const int len = (int)(se - p_seg) + 4;
+    const int64_t tile = p_seg / g.n0;
+    const int plane = (int)(p_seg % g.n0) - 2 + p_r;
+    const int slot = issued % NR;
     mbar_expect_tx(&bars[slot], SLOT * 8);
-    tma_load_plane(sm + slot * SLOT, &tin, &bars[slot], k0 + g.h - 2, j0 + g.h - 2,
-                   i0 - 2 + s + g.h);
+    tma_load_plane(sm + slot * SLOT, &tin, &bars[slot], (int)(tile % ntk) * TK + g.h - 2,
+                   (int)(tile / ntk) * TJ + g.h - 2, plane + g.h);
+    ++issued;
+    if (++p_r == len) { p_r = 0; p_seg = se; }
   };
+  int total_pos = 0;
+  for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) total_pos += (int)(S.seg_end(x) - x) + 4;
   if (tid == 0)
-    for (int s = 0; s < min(NR - 1, nseq); ++s) issue(s);
+    while (issued < total_pos && issued < NR) issue_next();
 
-  const int jj = j0 + tj, kk = k0 + tk;
-  const bool active = jj < g.n1 && kk < g.n2;
-  const int toff = (tj + 2) * PK + (tk + 2);
-
-  for (int t = 0; t < nsteps; ++t) {
-    if (t == 0) {
-      for (int s = 0; s < 5; ++s) {
-        mbar_wait(&bars[s % NR], (s / NR) & 1);
-        to_internal_energy(sm + (s % NR) * SLOT);
+  int w = 0;   // stream position of the current window start
+  for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) {
+    const int64_t se = S.seg_end(x);
+    const int64_t tile = x / g.n0;
+    const int k0 = (int)(tile % ntk) * TK, j0 = (int)(tile / ntk) * TJ;
+    const int jj = j0 + tj, kk = k0 + tk;
+    const bool active = jj < g.n1 && kk < g.n2;
+    const int toff = (tj + 2) * PK + (tk + 2);
+    const int nsteps = (int)(se - x);
+    double q1[5], q2[5];   // SN axis-0 queues
+    for (int t = 0; t < nsteps; ++t, ++w) {
+      const int first = t == 0 ? w : w + 4;
+      for (int pp = first; pp <= w + 4; ++pp) {
+        mbar_wait(&bars[pp % NR], (pp / NR) & 1);
+        to_internal_energy(sm + (pp % NR) * SLOT);
       }
-    } else {
-      const int s = t + 4;
-      mbar_wait(&bars[s % NR], (s / NR) & 1);
-      to_internal_energy(sm + (s % NR) * SLOT);
-    }
-    __syncthreads();
-    if (tid == 0 && t + 5 < nseq) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(t + 5);
-    }
+      __syncthreads();
+      if (tid == 0) {
+        if (issued < total_pos && issued < w + NR) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          while (issued < total_pos && issued < w + NR) issue_next();
+        }
+      }
+      SAcc a;
+#pragma unroll
+      for (int d = 0; d < 5; ++d) a.p[d] = sm + ((w + d) % NR) * SLOT + toff;
 
-    SAcc a;
+      if constexpr (kBuf) {
+        // axis-0 queues of D(u1,x1), D(u2,x2) at this column
+        if (t == 0) {
 #pragma unroll
-    for (int d = 0; d < 5; ++d) a.p[d] = sm + ((t + d) % NR) * SLOT + toff;
-    double r[NFIELDS];
+          for (int d = 0; d < 5; ++d) {
+            SAcc b;
+            b.p[2] = a.p[d];
+            q1[d] = d1<1, E_FIELD, U1, 0>(k, b);
+            q2[d] = d1<2, E_FIELD, U2, 0>(k, b);
+          }
+        } else {
 #pragma unroll
-    for (int f = 0; f < NFIELDS; ++f) r[f] = a.v(f, 0, 0, 0);   // r[RHOE_F] = rho*e
+          for (int d = 0; d < 4; ++d) { q1[d] = q1[d + 1]; q2[d] = q2[d + 1]; }
+          SAcc b;
+          b.p[2] = a.p[4];
+          q1[4] = d1<1, E_FIELD, U1, 0>(k, b);
+          q2[4] = d1<2, E_FIELD, U2, 0>(k, b);
+        }
+        // centre-plane buffers over the staged box
+        const double* c0 = sm + ((w + 2) % NR) * SLOT;
+        for (int xx = tid; xx < PLANE; xx += NT) {
+          const int r = xx / PK, cc = xx % PK;
+          SAcc b;
+#pragma unroll
+          for (int d = 0; d < 5; ++d) b.p[d] = sm + ((w + d) % NR) * SLOT + xx;
+          bufs[xx] = d1<0, E_FIELD, U0, 0>(k, b);
+          if (r >= 2 && r < TJ + 2) bufs[PLANE + xx] = d1<1, E_FIELD, U1, 0>(k, b);
+          if (cc >= 2 && cc < TK + 2) bufs[2 * PLANE + xx] = d1<2, E_FIELD, U2, 0>(k, b);
+        }
+        (void)c0;
+        __syncthreads();
+      }
 
-    const int i = i0 + t;
-    double R[5];
-    if constexpr (V == FDNS_SN) {
-      LocalProvider<SAcc> P(k, a);
-      residual_point<true>(k, P, r, R);
-    } else if constexpr (V == FDNS_RA) {
-      InlineProvider<SAcc> P(k, a);
-      residual_point<true>(k, P, r, R);
-    } else {  // SS / RS: stored velocity gradients from the work arrays
-      // inactive (edge) threads read a valid clamped column; never written
-      const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(min(jj, g.n1 - 1) + g.h) * g.s1 +
-                        (min(kk, g.n2 - 1) + g.h);
-      SSProvider<SAcc> P(k, a, work, c, g.fs, g.s0, g.s1);
-      residual_point<true>(k, P, r, R);
-    }
-    if (active) {
-      if constexpr (MODE == 0) {
-        emit<5>(out, g, i, jj, kk, R, 0);
-      } else {
-        const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(jj + g.h) * g.s1 + (kk + g.h);
-        double q[NFIELDS];
+      double r[NFIELDS];
 #pragma unroll
-        for (int f = 0; f < 5; ++f) q[f] = saved[f * g.fs + c] + coef * R[f];
-        primitives_point(k, q, q + 5);
-        emit<NFIELDS>(out, g, i, jj, kk, q, wrap_mask);
+      for (int f = 0; f < NFIELDS; ++f) r[f] = a.v(f, 0, 0, 0);   // r[RHOE_F] = rho*e
+      const int i = (int)(x % g.n0) + t;
+      double R[5];
+      if constexpr (V == FDNS_SN) {
+        TiledLocalProvider P(k, a, q1, q2, bufs + toff, bufs + PLANE + toff,
+                             bufs + 2 * PLANE + toff);
+        residual_point<true>(k, P, r, R);
+      } else if constexpr (V == FDNS_RA) {
+        InlineProvider<SAcc> P(k, a);
+        residual_point<true>(k, P, r, R);
+      } else {  // SS / RS: stored velocity gradients from the work arrays
+        // inactive (edge) threads read a valid clamped column; never written
+        const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(min(jj, g.n1 - 1) + g.h) * g.s1 +
+                          (min(kk, g.n2 - 1) + g.h);
+        SSProvider<SAcc, V == FDNS_RS> P(k, a, work, c, g.fs, g.s0, g.s1);
+        residual_point<true>(k, P, r, R);
+      }
+      if (active) {
+        if constexpr (MODE == 0) {
+          emit<5>(out, g, i, jj, kk, R, 0);
+        } else {
+          const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(jj + g.h) * g.s1 + (kk + g.h);
+          double q[NFIELDS];
+#pragma unroll
+          for (int f = 0; f < 5; ++f) q[f] = saved[f * g.fs + c] + coef * R[f];
+          primitives_point(k, q, q + 5);
+          emit<NFIELDS>(out, g, i, jj, kk, q, wrap_mask);
+        }
       }
     }
+    w += 4;   // the segment's trailing positions
   }
 }
 
