@@ -93,6 +93,11 @@ int32_t fdns_stage(int32_t variant, const double* in, const double* saved,
  * row pitch allows).  Both paths are parity-tested. */
 void fdns_set_kernel_path(int32_t point_only);
 
+/* Test hook: force the persistent tiled kernels onto `ctas` CTAs (0 =
+ * default, one per SM) -- small grids then cross many tile/segment
+ * boundaries inside one CTA. */
+void fdns_set_tiled_grid(int32_t ctas);
+
 /* Device reduction of the diagnostics of a state bundle (halos current):
  * out[0] = sum 0.5*rho*|u|^2, out[1] = sum 0.5*rho*|omega|^2, with rho from
  * `state` and the velocities (fields 5-7) from `prim_state` (NULL = state;

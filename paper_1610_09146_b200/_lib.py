@@ -52,6 +52,7 @@ EXPORTS = {
     "fdns_stage": (_I, [_I, _VP, _VP, _VP, _VP, ctypes.c_double, _I,
                         ctypes.POINTER(Problem), _VP]),
     "fdns_set_kernel_path": (None, [_I]),
+    "fdns_set_tiled_grid": (None, [_I]),
     "fdns_diag_partials_size": (_I, [ctypes.POINTER(Problem)]),
     "fdns_reduce_diag": (_I, [_VP, _VP, _VP, _VP, ctypes.POINTER(Problem),
                               _VP]),

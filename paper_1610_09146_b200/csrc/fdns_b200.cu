@@ -23,6 +23,7 @@ namespace {
 
 thread_local std::string g_err;
 bool g_force_point = false;   // test hook: run the point kernels everywhere
+int g_tiled_ctas = 0;         // test hook: force the tiled grid size (0 = one per SM)
 std::atomic<long long> g_launches{0};
 inline void count(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
@@ -452,7 +453,8 @@ int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const
   const int ntj = (g.n1 + tiled::TJ - 1) / tiled::TJ;
   const int64_t total = (int64_t)ntk * ntj * g.n0;
   // one persistent CTA per SM, each at least ~4 plane steps
-  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(num_sms(), total / 4));
+  int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(num_sms(), total / 4));
+  if (g_tiled_ctas > 0) ctas = std::min<int64_t>(g_tiled_ctas, total);
   tiled::k_stage_tiled<V, MODE><<<(unsigned)ctas, tiled::NT, smem, s>>>(
       m, work, saved, out, k, g, coef, ntk, total, wrap);
   return 0;
@@ -529,6 +531,8 @@ int32_t fdns_abi_version(void) { return 1; }
 int64_t fdns_launch_count(void) { return g_launches.load(); }
 
 void fdns_set_kernel_path(int32_t point_only) { g_force_point = point_only != 0; }
+
+void fdns_set_tiled_grid(int32_t ctas) { g_tiled_ctas = ctas; }
 
 int32_t fdns_workarray_count(int32_t variant) {
   switch (variant) {

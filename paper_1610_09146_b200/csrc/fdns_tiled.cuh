@@ -56,8 +56,13 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Bounded wait: a producer/consumer bug must surface as a kernel error, not
+// as a hung GPU.  ~4e9 cycles is seconds; a healthy wait is microseconds.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
   while (!mbar_try(bar, parity)) {
+    if (clock64() - t0 > 4000000000LL) __trap();
   }
 }
 __device__ __forceinline__ void tma_load_plane(double* dst, const CUtensorMap* map, uint64_t* bar,
@@ -245,6 +250,15 @@ __global__ void __launch_bounds__(NT, 1)
     const int nsteps = (int)(se - x);
     double q1[5], q2[5];   // SN axis-0 queues
     for (int t = 0; t < nsteps; ++t, ++w) {
+      if (t == 0 && w > 0) {
+        // segment change: the new window needs 5 fresh planes; refill the
+        // ring once every thread is done with the previous segment's slots
+        __syncthreads();
+        if (tid == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          while (issued < total_pos && issued < w + NR) issue_next();
+        }
+      }
       const int first = t == 0 ? w : w + 4;
       for (int pp = first; pp <= w + 4; ++pp) {
         mbar_wait(&bars[pp % NR], (pp / NR) & 1);

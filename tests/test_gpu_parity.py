@@ -263,3 +263,37 @@ def test_workarray_allocations_match_budget(variant):
     del ev
     gc.collect()
     assert fd.live_field_count() == base
+
+
+# ------------------------------------------------- kernel-path coverage
+@pytest.fixture
+def kernel_path():
+    from paper_1610_09146_b200 import _lib
+    lib = _lib.load()
+    yield lib
+    lib.fdns_set_kernel_path(0)
+    lib.fdns_set_tiled_grid(0)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("ctas", [3, 7, 13])
+def test_tiled_segment_transitions(kernel_path, variant, ctas):
+    """Force the persistent tiled kernel onto few CTAs so each walks several
+    (tile, plane-range) segments; results stay bitwise equal to the
+    one-thread-per-point path."""
+    npts = (21, 20, 34)
+    F = npo.state_from_primitives(npts, CO, np.ones(npts) + 0.01 * np.arange(
+        np.prod(npts)).reshape(npts) / np.prod(npts),
+        [0.1 * np.sin(np.arange(np.prod(npts)).reshape(npts))] * 3,
+        np.full(npts, 70.0))
+    g = grid_of(npts)
+    cons = npo.interior(F[:5], 2)
+    kernel_path.fdns_set_kernel_path(1)
+    a = state_from_cons(g, cons)
+    fd.run(a, fd.RKScheme(dt=1e-3), fd.ResidualEvaluator(g, C, variant), 2)
+    want = host_cons(a)
+    kernel_path.fdns_set_kernel_path(0)
+    kernel_path.fdns_set_tiled_grid(ctas)
+    b = state_from_cons(g, cons)
+    fd.run(b, fd.RKScheme(dt=1e-3), fd.ResidualEvaluator(g, C, variant), 2)
+    assert np.array_equal(host_cons(b), want)
