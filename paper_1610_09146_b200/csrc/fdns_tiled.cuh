@@ -144,8 +144,14 @@ __device__ __forceinline__ void to_internal_energy(double* slot) {
 // over the staged box, so the in-plane mixed terms read 4 values each
 // instead of re-expanding 4 inner stencils (same stencil shape at every
 // point: bitwise equal to the reference's re-expansion, codegen.py:97-102).
+// Double-buffered (step parity), so the buffers of step t are written while
+// slower threads may still read those of step t-1: one barrier per step.
 constexpr int NBUF = 3;
-constexpr int SMEM_BYTES_SN = NR * SLOT * 8 + NBUF * PLANE * 8 + 128;
+constexpr int BU1_N = TJ * PK;          // D(u1,x1): interior rows, all columns
+constexpr int BU2_N = PJ * TK;          // D(u2,x2): all rows, interior columns
+constexpr int BUF_WORK = PLANE + BU1_N + BU2_N;
+constexpr int SMEM_BYTES_SN = NR * SLOT * 8 + 2 * NBUF * PLANE * 8 + 128;
+static_assert(SMEM_BYTES_SN <= 232448, "SN tile exceeds the 227 KB shared-memory limit");
 
 // SN provider over the staged tile: every distinct derivative once (LOCAL),
 // diagonal velocity gradients and the six mixed terms from the axis-0
@@ -202,8 +208,8 @@ __global__ void __launch_bounds__(NT, 1)
                   int64_t total_steps, int wrap_mask) {
   extern __shared__ __align__(128) double sm[];
   constexpr bool kBuf = (V == FDNS_SN);
-  double* bufs = sm + NR * SLOT;   // NBUF planes (SN only)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NR * SLOT + (kBuf ? NBUF * PLANE : 0));
+  double* bufs0 = sm + NR * SLOT;   // 2 x NBUF planes (SN only)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NR * SLOT + (kBuf ? 2 * NBUF * PLANE : 0));
   const int tid = threadIdx.x;
   const int tk = tid % TK, tj = tid / TK;
   Segments S{blockIdx.x * total_steps / gridDim.x, (blockIdx.x + 1) * total_steps / gridDim.x,
@@ -264,6 +270,25 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_wait(&bars[pp % NR], (pp / NR) & 1);
         to_internal_energy(sm + (pp % NR) * SLOT);
       }
+      double* bufs = bufs0 + (w & 1) * NBUF * PLANE;
+      if constexpr (kBuf) {
+        // centre-plane buffers over the staged box (u0..u2 are untouched by
+        // the energy conversion, so no barrier is needed before this)
+        for (int xx = tid; xx < BUF_WORK; xx += NT) {
+          int pos, which;
+          if (xx < PLANE) { pos = xx; which = 0; }
+          else if (xx < PLANE + BU1_N) { pos = 2 * PK + (xx - PLANE); which = 1; }
+          else { const int y = xx - PLANE - BU1_N; pos = (y / TK) * PK + 2 + y % TK; which = 2; }
+          SAcc b;
+#pragma unroll
+          for (int d = 0; d < 5; ++d) b.p[d] = sm + ((w + d) % NR) * SLOT + pos;
+          double val;
+          if (which == 0) val = d1<0, E_FIELD, U0, 0>(k, b);
+          else if (which == 1) val = d1<1, E_FIELD, U1, 0>(k, b);
+          else val = d1<2, E_FIELD, U2, 0>(k, b);
+          bufs[which * PLANE + pos] = val;
+        }
+      }
       __syncthreads();
       if (tid == 0) {
         if (issued < total_pos && issued < w + NR) {
@@ -293,19 +318,6 @@ __global__ void __launch_bounds__(NT, 1)
           q1[4] = d1<1, E_FIELD, U1, 0>(k, b);
           q2[4] = d1<2, E_FIELD, U2, 0>(k, b);
         }
-        // centre-plane buffers over the staged box
-        const double* c0 = sm + ((w + 2) % NR) * SLOT;
-        for (int xx = tid; xx < PLANE; xx += NT) {
-          const int r = xx / PK, cc = xx % PK;
-          SAcc b;
-#pragma unroll
-          for (int d = 0; d < 5; ++d) b.p[d] = sm + ((w + d) % NR) * SLOT + xx;
-          bufs[xx] = d1<0, E_FIELD, U0, 0>(k, b);
-          if (r >= 2 && r < TJ + 2) bufs[PLANE + xx] = d1<1, E_FIELD, U1, 0>(k, b);
-          if (cc >= 2 && cc < TK + 2) bufs[2 * PLANE + xx] = d1<2, E_FIELD, U2, 0>(k, b);
-        }
-        (void)c0;
-        __syncthreads();
       }
 
       double r[NFIELDS];
