@@ -324,6 +324,14 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int f = 0; f < NFIELDS; ++f) r[f] = a.v(f, 0, 0, 0);   // r[RHOE_F] = rho*e
       const int i = (int)(x % g.n0) + t;
+      // issue the saved-state loads now; they land while the residual runs
+      double sv[5];
+      if constexpr (MODE == 1) {
+        const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(min(jj, g.n1 - 1) + g.h) * g.s1 +
+                          (min(kk, g.n2 - 1) + g.h);
+#pragma unroll
+        for (int f = 0; f < 5; ++f) sv[f] = saved[f * g.fs + c];
+      }
       double R[5];
       if constexpr (V == FDNS_SN) {
         TiledLocalProvider P(k, a, q1, q2, bufs + toff, bufs + PLANE + toff,
@@ -345,8 +353,9 @@ __global__ void __launch_bounds__(NT, 1)
         } else {
           const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(jj + g.h) * g.s1 + (kk + g.h);
           double q[NFIELDS];
+          (void)c;
 #pragma unroll
-          for (int f = 0; f < 5; ++f) q[f] = saved[f * g.fs + c] + coef * R[f];
+          for (int f = 0; f < 5; ++f) q[f] = sv[f] + coef * R[f];
           primitives_point(k, q, q + 5);
           emit<NFIELDS>(out, g, i, jj, kk, q, wrap_mask);
         }
