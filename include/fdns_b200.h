@@ -88,10 +88,12 @@ int32_t fdns_stage(int32_t variant, const double* in, const double* saved,
                    double* out, double* work, double coef, int32_t wrap_mask,
                    const fdns_problem* pb, void* stream);
 
-/* Test hook: 1 = run every variant on the one-thread-per-point kernels
- * (global-memory taps), 0 = default (TMA-staged tiled kernels where the
- * row pitch allows).  Both paths are parity-tested. */
-void fdns_set_kernel_path(int32_t point_only);
+/* Test hook selecting the kernel family: 0 = default (TMA-staged tiled
+ * kernels where the row pitch allows; SN on two warp groups per point),
+ * 1 = one-thread-per-point kernels (global-memory taps) for every variant,
+ * 2 = default but SN on the single-group tiled kernel.  All paths are
+ * parity-tested. */
+void fdns_set_kernel_path(int32_t path);
 
 /* Test hook: force the persistent tiled kernels onto `ctas` CTAs (0 =
  * default, one per SM) -- small grids then cross many tile/segment

@@ -13,6 +13,7 @@
 #include "../../include/fdns_b200.h"
 #include "fdns_math.cuh"
 #include "fdns_tiled.cuh"
+#include "fdns_sn2.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -22,7 +23,7 @@ using namespace fdns;
 namespace {
 
 thread_local std::string g_err;
-bool g_force_point = false;   // test hook: run the point kernels everywhere
+int g_kernel_path = 0;        // test hook: 0 default, 1 point kernels, 2 single-group SN
 int g_tiled_ctas = 0;         // test hook: force the tiled grid size (0 = one per SM)
 std::atomic<long long> g_launches{0};
 inline void count(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
@@ -461,15 +462,37 @@ int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const
 }
 
 template <int MODE>
+int launch_sn2(const CUtensorMap& m, const double* saved, double* out, const Coef& k,
+               const Geom& g, double coef, int wrap, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sn2::k_stage_sn2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         sn2::SMEM_BYTES);
+    attr = true;
+  }
+  const int ntk = (g.n2 + tiled::TK - 1) / tiled::TK;
+  const int ntj = (g.n1 + tiled::TJ - 1) / tiled::TJ;
+  const int64_t total = (int64_t)ntk * ntj * g.n0;
+  int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(num_sms(), total / 4));
+  if (g_tiled_ctas > 0) ctas = std::min<int64_t>(g_tiled_ctas, total);
+  sn2::k_stage_sn2<MODE><<<(unsigned)ctas, sn2::NT, sn2::SMEM_BYTES, s>>>(m, saved, out, k, g, coef,
+                                                                          ntk, total, wrap);
+  return 0;
+}
+
+template <int MODE>
 int launch_residual(int variant, const double* in, const double* saved, double* out,
                     double* work, const Coef& k, const Geom& g, double coef, int wrap,
                     cudaStream_t s) {
   CUtensorMap m;
-  if (variant != FDNS_BL && !g_force_point && plane_map(&m, in, g)) {
+  if (variant != FDNS_BL && g_kernel_path != 1 && plane_map(&m, in, g)) {
     switch (variant) {
       case FDNS_RA: launch_tiled_v<FDNS_RA, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
       case FDNS_RS: launch_tiled_v<FDNS_RS, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
-      case FDNS_SN: launch_tiled_v<FDNS_SN, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
+      case FDNS_SN:
+        if (g_kernel_path == 2) launch_tiled_v<FDNS_SN, MODE>(m, saved, out, work, k, g, coef, wrap, s);
+        else launch_sn2<MODE>(m, saved, out, k, g, coef, wrap, s);
+        break;
       case FDNS_SS: launch_tiled_v<FDNS_SS, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
       default: return fail("unknown variant");
     }
@@ -530,7 +553,7 @@ int32_t fdns_abi_version(void) { return 1; }
 
 int64_t fdns_launch_count(void) { return g_launches.load(); }
 
-void fdns_set_kernel_path(int32_t point_only) { g_force_point = point_only != 0; }
+void fdns_set_kernel_path(int32_t path) { g_kernel_path = path; }
 
 void fdns_set_tiled_grid(int32_t ctas) { g_tiled_ctas = ctas; }
 

@@ -282,18 +282,32 @@ __device__ __forceinline__ double viscous(const Coef& k, const Pv& P) {
          k.inv_Re * G(J2, S_U2 + I) + k.c13 * X(J2, I);
 }
 
+// Momentum i, split into the chain prefix -(0.5*(conv)) - D(p,x_i) and the
+// viscous suffix (terms.py:164-165, one flat left-to-right chain; splitting
+// a chain after a term keeps every rounding step, so prefix + suffix is
+// bitwise the full chain).
 template <int I, class Pv>
-__device__ __forceinline__ double momentum(const Coef& k, const Pv& P, const double* r) {
+__device__ __forceinline__ double momentum_prefix(const Coef& k, const Pv& P, const double* r) {
   constexpr int SALT = 4 + I;
   const double rui = r[RU0 + I];
   const double conv = G(0, S_RUU + I) + r[U0] * G(0, S_RU + I) + rui * G(0, S_U + 0) +
                       G(1, S_RUU + I) + r[U1] * G(1, S_RU + I) + rui * G(1, S_U + 1) +
                       G(2, S_RUU + I) + r[U2] * G(2, S_RU + I) + rui * G(2, S_U + 2);
+  return -(0.5 * conv) - G(I, S_P);
+}
+
+template <int I, class Pv>
+__device__ __forceinline__ double momentum_suffix(const Coef& k, const Pv& P, double pre) {
+  constexpr int SALT = 10 + I;
   constexpr int J1 = I == 0 ? 1 : 0;
   constexpr int J2 = I == 2 ? 1 : 2;
-  // -(0.5*(conv)) - D(p,x_i) + viscous terms, flat chain (terms.py:164-165)
-  return -(0.5 * conv) - G(I, S_P) + k.c43 * G(I, S_U2 + I) + k.inv_Re * G(J1, S_U2 + I) +
-         k.c13 * X(J1, I) + k.inv_Re * G(J2, S_U2 + I) + k.c13 * X(J2, I);
+  return pre + k.c43 * G(I, S_U2 + I) + k.inv_Re * G(J1, S_U2 + I) + k.c13 * X(J1, I) +
+         k.inv_Re * G(J2, S_U2 + I) + k.c13 * X(J2, I);
+}
+
+template <int I, class Pv>
+__device__ __forceinline__ double momentum(const Coef& k, const Pv& P, const double* r) {
+  return momentum_suffix<I>(k, P, momentum_prefix<I>(k, P, r));
 }
 
 template <int I, int J, class Pv>
@@ -306,39 +320,52 @@ __device__ __forceinline__ double tau(const Coef& k, const Pv& P) {
     return k.inv_Re * (G(J, S_U + I) + G(I, S_U + J));
 }
 
+// mass (terms.py:151-156)
+template <class Pv>
+__device__ __forceinline__ double mass_residual(const Coef& k, const Pv& P, const double* r) {
+  constexpr int SALT = 13;
+  const double acc = G(0, S_RU + 0) + r[U0] * G(0, S_RHO) + r[RHO] * G(0, S_U + 0) +
+                     G(1, S_RU + 1) + r[U1] * G(1, S_RHO) + r[RHO] * G(1, S_U + 1) +
+                     G(2, S_RU + 2) + r[U2] * G(2, S_RHO) + r[RHO] * G(2, S_U + 2);
+  return -(0.5 * acc);
+}
+
+// energy (terms.py:167-183), split after the nine stress-work terms
+template <bool RHOE_INTERNAL, class Pv>
+__device__ __forceinline__ double energy_prefix(const Coef& k, const Pv& P, const double* r) {
+  constexpr int SALT = 14;
+  const double rhoe = RHOE_INTERNAL ? r[RHOE_F]
+                                    : r[RHOE_F] - 0.5 * (r[RU0] * r[U0] + r[RU1] * r[U1] +
+                                                         r[RU2] * r[U2]);
+  const double conv = G(0, S_RHOEU) + r[U0] * G(0, S_RHOE) + rhoe * G(0, S_U + 0) +
+                      G(1, S_RHOEU) + r[U1] * G(1, S_RHOE) + rhoe * G(1, S_U + 1) +
+                      G(2, S_RHOEU) + r[U2] * G(2, S_RHOE) + rhoe * G(2, S_U + 2);
+  const double pwork = G(0, S_UP) + G(1, S_UP) + G(2, S_UP);
+  const double heat = k.heat * (G(0, S_T2) + G(1, S_T2) + G(2, S_T2));
+  return -(0.5 * conv) - (pwork) + heat +
+         tau<0, 0>(k, P) * G(0, S_U + 0) + tau<0, 1>(k, P) * G(1, S_U + 0) +
+         tau<0, 2>(k, P) * G(2, S_U + 0) + tau<1, 0>(k, P) * G(0, S_U + 1) +
+         tau<1, 1>(k, P) * G(1, S_U + 1) + tau<1, 2>(k, P) * G(2, S_U + 1) +
+         tau<2, 0>(k, P) * G(0, S_U + 2) + tau<2, 1>(k, P) * G(1, S_U + 2) +
+         tau<2, 2>(k, P) * G(2, S_U + 2);
+}
+
+template <class Pv>
+__device__ __forceinline__ double energy_suffix(const Coef& k, const Pv& P, const double* r,
+                                                double pre) {
+  return pre + r[U0] * (viscous<0>(k, P)) + r[U1] * (viscous<1>(k, P)) +
+         r[U2] * (viscous<2>(k, P));
+}
+
 // RHOE_INTERNAL: r[RHOE_F] already holds rho*e (staged-tile accessors).
 template <bool RHOE_INTERNAL = false, class Pv>
 __device__ __forceinline__ void residual_point(const Coef& k, const Pv& P, const double* r,
                                                double* out) {
-  constexpr int SALT = 0;
-  // mass (terms.py:151-156)
-  {
-    const double acc = G(0, S_RU + 0) + r[U0] * G(0, S_RHO) + r[RHO] * G(0, S_U + 0) +
-                       G(1, S_RU + 1) + r[U1] * G(1, S_RHO) + r[RHO] * G(1, S_U + 1) +
-                       G(2, S_RU + 2) + r[U2] * G(2, S_RHO) + r[RHO] * G(2, S_U + 2);
-    out[0] = -(0.5 * acc);
-  }
+  out[0] = mass_residual(k, P, r);
   out[1] = momentum<0>(k, P, r);
   out[2] = momentum<1>(k, P, r);
   out[3] = momentum<2>(k, P, r);
-  // energy (terms.py:167-183)
-  {
-    const double rhoe = RHOE_INTERNAL ? r[RHOE_F]
-                                      : r[RHOE_F] - 0.5 * (r[RU0] * r[U0] + r[RU1] * r[U1] +
-                                                           r[RU2] * r[U2]);
-    const double conv = G(0, S_RHOEU) + r[U0] * G(0, S_RHOE) + rhoe * G(0, S_U + 0) +
-                        G(1, S_RHOEU) + r[U1] * G(1, S_RHOE) + rhoe * G(1, S_U + 1) +
-                        G(2, S_RHOEU) + r[U2] * G(2, S_RHOE) + rhoe * G(2, S_U + 2);
-    const double pwork = G(0, S_UP) + G(1, S_UP) + G(2, S_UP);
-    const double heat = k.heat * (G(0, S_T2) + G(1, S_T2) + G(2, S_T2));
-    out[4] = -(0.5 * conv) - (pwork) + heat +
-             tau<0, 0>(k, P) * G(0, S_U + 0) + tau<0, 1>(k, P) * G(1, S_U + 0) +
-             tau<0, 2>(k, P) * G(2, S_U + 0) + tau<1, 0>(k, P) * G(0, S_U + 1) +
-             tau<1, 1>(k, P) * G(1, S_U + 1) + tau<1, 2>(k, P) * G(2, S_U + 1) +
-             tau<2, 0>(k, P) * G(0, S_U + 2) + tau<2, 1>(k, P) * G(1, S_U + 2) +
-             tau<2, 2>(k, P) * G(2, S_U + 2) + r[U0] * (viscous<0>(k, P)) +
-             r[U1] * (viscous<1>(k, P)) + r[U2] * (viscous<2>(k, P));
-  }
+  out[4] = energy_suffix(k, P, r, energy_prefix<RHOE_INTERNAL>(k, P, r));
 }
 #undef G
 #undef X

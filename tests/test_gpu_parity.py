@@ -297,3 +297,22 @@ def test_tiled_segment_transitions(kernel_path, variant, ctas):
     b = state_from_cons(g, cons)
     fd.run(b, fd.RKScheme(dt=1e-3), fd.ResidualEvaluator(g, C, variant), 2)
     assert np.array_equal(host_cons(b), want)
+
+
+@pytest.mark.parametrize("ctas", [0, 5])
+def test_sn_kernel_families_agree(kernel_path, ctas):
+    """SN on two warp groups (default), on one (path 2) and on the point
+    kernels (path 1): bitwise equal after two RK3 steps."""
+    npts = (19, 24, 40)
+    F = npo.manufactured(npts, CO)
+    g = grid_of(npts)
+    cons = npo.interior(F[:5], 2)
+    finals = []
+    for path in (1, 2, 0):
+        kernel_path.fdns_set_kernel_path(path)
+        kernel_path.fdns_set_tiled_grid(ctas)
+        st = state_from_cons(g, cons)
+        fd.run(st, fd.RKScheme(dt=1e-3), fd.ResidualEvaluator(g, C, "SN"), 2)
+        finals.append(host_cons(st))
+    assert np.array_equal(finals[0], finals[1])
+    assert np.array_equal(finals[0], finals[2])

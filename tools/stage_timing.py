@@ -22,11 +22,12 @@ def main():
     ap.add_argument("--sizes", default="64,128,256")
     ap.add_argument("--variants", default="SN,SS,RA,BL")
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--point", action="store_true", help="point kernels only")
+    ap.add_argument("--path", type=int, default=0,
+                    help="kernel family: 0 default, 1 point kernels, 2 single-group SN")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     lib = _lib.load()
-    lib.fdns_set_kernel_path(1 if a.point else 0)
+    lib.fdns_set_kernel_path(a.path)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     c = fd.PhysicalConstants()
     out = {}
