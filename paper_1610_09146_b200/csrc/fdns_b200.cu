@@ -421,7 +421,7 @@ bool plane_map(CUtensorMap* m, const double* base, const Geom& g) {
   cuuint64_t dims[4] = {(cuuint64_t)P2, (cuuint64_t)P1, (cuuint64_t)P0, (cuuint64_t)NFIELDS};
   cuuint64_t strides[3] = {(cuuint64_t)(P2 * 8), (cuuint64_t)(P1 * P2 * 8),
                            (cuuint64_t)(g.fs * 8)};
-  cuuint32_t box[4] = {tiled::PK, tiled::PJ, 1, NFIELDS};
+  cuuint32_t box[4] = {tiled::PK, tiled::PJ, 1, tiled::NLOAD};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -8,17 +8,15 @@
 //
 // Each point is owned by a thread in warp group A (warps 0-7) and one in
 // group B (warps 8-15); groups are whole warps, so nothing diverges.
-//   B: chain prefixes of momentum 1 and 2 (convection + pressure gradient)
-//      and of energy (convection, pressure work, heat conduction, the nine
-//      stress-work terms) -> 3 doubles per point through shared memory.
-//   A: mass, momentum 0, the viscous suffixes of momentum 1/2, the energy
-//      suffix u_i*(viscous_i), the RK update and the primitives.
-// Splitting a left-to-right chain after a term keeps every rounding step,
-// so the result is bitwise that of residual_point (terms.py:151-183).
+//   A: mass and the three momentum residuals, their RK update and u = rhou/rho
+//   B: the energy residual and its RK update
+// The two groups are independent within a step (the energy residual needs
+// the viscous terms too, so B evaluates them itself); p and T are derived on
+// arrival of each staged plane instead of being written by the epilogue.
 // Each group evaluates every derivative it uses once (SN, LOCAL semantics
 // per thread; the compiler CSEs repeated uses); the diagonal velocity
 // gradients and mixed terms come from the shared centre-plane buffers and
-// group A's axis-0 queues.
+// the axis-0 queues.
 #pragma once
 #include "fdns_tiled.cuh"
 
@@ -41,7 +39,7 @@ constexpr int NT = 2 * NPT;      // threads (512)
 // (pitch TK); double-buffered by step parity
 constexpr int B0_N = PLANE, B1_N = TJ * PK, B2_N = PJ * TK;
 constexpr int BSET = B0_N + B1_N + B2_N;
-constexpr int NXCH = 3;          // prefixes handed from B to A
+constexpr int NXCH = 0;
 constexpr int SMEM_BYTES = NR * SLOT * 8 + 2 * BSET * 8 + NXCH * NPT * 8 + 64;
 static_assert(SMEM_BYTES <= 232448, "sn2 tile exceeds the 227 KB shared-memory limit");
 
@@ -88,8 +86,7 @@ __global__ void __launch_bounds__(NT, 1)
                 Coef k, Geom g, double coef, int ntk, int64_t total_steps, int wrap_mask) {
   extern __shared__ __align__(128) double sm[];
   double* bset0 = sm + NR * SLOT;
-  double* xch = bset0 + 2 * BSET;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xch + NXCH * NPT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bset0 + 2 * BSET);
   const int tid = threadIdx.x;
   const bool groupB = tid >= NPT;
   const int pt = groupB ? tid - NPT : tid;
@@ -113,7 +110,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int64_t tile = p_seg / g.n0;
     const int plane = (int)(p_seg % g.n0) - 2 + p_r;
     const int slot = issued % NR;
-    tiled::mbar_expect_tx(&bars[slot], SLOT * 8);
+    tiled::mbar_expect_tx(&bars[slot], tiled::LOAD_BYTES);
     tiled::tma_load_plane(sm + slot * SLOT, &tin, &bars[slot], (int)(tile % ntk) * TK + g.h - 2,
                           (int)(tile / ntk) * TJ + g.h - 2, plane + g.h);
     ++issued;
@@ -145,14 +142,7 @@ __global__ void __launch_bounds__(NT, 1)
       const int first = t == 0 ? w : w + 4;
       for (int pp = first; pp <= w + 4; ++pp) {
         tiled::mbar_wait(&bars[pp % NR], (pp / NR) & 1);
-        for (int xx = tid; xx < PLANE; xx += NT) {   // rhoE -> rho*e
-          double* slot = sm + (pp % NR) * SLOT;
-          slot[RHOE_F * PLANE + xx] =
-              slot[RHOE_F * PLANE + xx] -
-              0.5 * (slot[RU0 * PLANE + xx] * slot[U0 * PLANE + xx] +
-                     slot[RU1 * PLANE + xx] * slot[U1 * PLANE + xx] +
-                     slot[RU2 * PLANE + xx] * slot[U2 * PLANE + xx]);
-        }
+        tiled::stage_arrival(k, sm + (pp % NR) * SLOT, tid, NT);
       }
       double* bs = bset0 + (w & 1) * BSET;
       for (int xx = tid; xx < BSET; xx += NT) {      // centre-plane buffers
@@ -170,7 +160,7 @@ __global__ void __launch_bounds__(NT, 1)
       SAcc a;
 #pragma unroll
       for (int d = 0; d < 5; ++d) a.p[d] = sm + ((w + d) % NR) * SLOT + toff;
-      if (!groupB) {
+      {   // axis-0 queues of D(u1,x1), D(u2,x2) (both groups use the mixed terms)
         if (t == 0) {
 #pragma unroll
           for (int d = 0; d < 5; ++d) {
@@ -200,36 +190,41 @@ __global__ void __launch_bounds__(NT, 1)
       const int i = (int)(x % g.n0) + t;
       const LazyProvider P{k, a, q1, q2, bs + toff, bs + B0_N + tj * PK + tk + 2,
                            bs + B0_N + B1_N + (tj + 2) * TK + tk};
+      const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(min(jj, g.n1 - 1) + g.h) * g.s1 +
+                        (min(kk, g.n2 - 1) + g.h);
       if (groupB) {
-        xch[0 * NPT + pt] = momentum_prefix<1>(k, P, r);
-        xch[1 * NPT + pt] = momentum_prefix<2>(k, P, r);
-        xch[2 * NPT + pt] = energy_prefix<true>(k, P, r);
-        asm volatile("bar.arrive 1, %0;" ::"n"(NT) : "memory");
-      } else {
-        const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(min(jj, g.n1 - 1) + g.h) * g.s1 +
-                          (min(kk, g.n2 - 1) + g.h);
-        double sv[5];
-        if constexpr (MODE == 1) {
-#pragma unroll
-          for (int f = 0; f < 5; ++f) sv[f] = saved[f * g.fs + c];
-        }
-        double R[5];
-        R[0] = mass_residual(k, P, r);
-        R[1] = momentum<0>(k, P, r);
-        // the suffix terms first (independent of B), then wait for B
-        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
-        R[2] = momentum_suffix<1>(k, P, xch[0 * NPT + pt]);
-        R[3] = momentum_suffix<2>(k, P, xch[1 * NPT + pt]);
-        R[4] = energy_suffix(k, P, r, xch[2 * NPT + pt]);
+        double sv = 0.0;
+        if constexpr (MODE == 1) sv = saved[RHOE_F * g.fs + c];
+        const double RE = energy_suffix(k, P, r, energy_prefix<true>(k, P, r));
         if (active) {
           if constexpr (MODE == 0) {
-            tiled::emit<5>(out, g, i, jj, kk, R, 0);
+            tiled::emit<1>(out + RHOE_F * g.fs, g, i, jj, kk, &RE, 0);
           } else {
-            double q[NFIELDS];
+            const double qe = sv + coef * RE;
+            tiled::emit<1>(out + RHOE_F * g.fs, g, i, jj, kk, &qe, wrap_mask);
+          }
+        }
+      } else {
+        double sv[4];
+        if constexpr (MODE == 1) {
 #pragma unroll
-            for (int f = 0; f < 5; ++f) q[f] = sv[f] + coef * R[f];
-            primitives_point(k, q, q + 5);
-            tiled::emit<NFIELDS>(out, g, i, jj, kk, q, wrap_mask);
+          for (int f = 0; f < 4; ++f) sv[f] = saved[f * g.fs + c];
+        }
+        double R[4];
+        R[0] = mass_residual(k, P, r);
+        R[1] = momentum<0>(k, P, r);
+        R[2] = momentum<1>(k, P, r);
+        R[3] = momentum<2>(k, P, r);
+        if (active) {
+          if constexpr (MODE == 0) {
+            tiled::emit<4>(out, g, i, jj, kk, R, 0);
+          } else {
+            double q[8];
+#pragma unroll
+            for (int f = 0; f < 4; ++f) q[f] = sv[f] + coef * R[f];
+            const double u[3] = {q[RU0] / q[RHO], q[RU1] / q[RHO], q[RU2] / q[RHO]};
+            tiled::emit<4>(out, g, i, jj, kk, q, wrap_mask);
+            tiled::emit<3>(out + U0 * g.fs, g, i, jj, kk, u, wrap_mask);
           }
         }
       }

@@ -29,6 +29,10 @@ constexpr int TK = 32, TJ = 8, NT = TK * TJ;
 constexpr int PK = TK + 4, PJ = TJ + 4;
 constexpr int PLANE = PK * PJ;          // doubles per field per plane slot
 constexpr int SLOT = NFIELDS * PLANE;   // doubles per plane slot
+constexpr int NLOAD = 8;                // fields TMA-staged per plane (rho..u2);
+                                        // p, T are derived on arrival
+constexpr uint32_t LOAD_BYTES = NLOAD * PLANE * 8;
+constexpr int NOUT_STAGE = 8;           // fields a fused stage writes (cons + u)
 constexpr int NR = 6;                   // ring depth: 5-plane window + 1 prefetch
 constexpr int SMEM_BYTES = NR * SLOT * 8 + 128;
 
@@ -129,15 +133,35 @@ __device__ __forceinline__ void emit(double* out, const Geom& g, int i, int j, i
   }
 }
 
-// rhoE -> rho*e in one staged plane slot (all PLANE points of the box).
-__device__ __forceinline__ void to_internal_energy(double* slot) {
-  for (int x = threadIdx.x; x < PLANE; x += NT) {
+// Arrival conversion of one staged plane slot (all PLANE points of the box):
+// rhoE -> rho*e = rhoE - 0.5*(rhou.u) (terms.py:39), then the primitive
+// expressions of the reference (physics.py:195-202): p = gm1*rho*e (the same
+// intermediate the reference forms), T = (gM2*p)/rho.  Bitwise the values
+// the primitives pass would have stored.
+__device__ __forceinline__ void stage_arrival(const Coef& k, double* slot, int tid, int nthreads) {
+  for (int x = tid; x < PLANE; x += nthreads) {
+    const double rho = slot[RHO * PLANE + x];
     const double e = slot[RHOE_F * PLANE + x] -
                      0.5 * (slot[RU0 * PLANE + x] * slot[U0 * PLANE + x] +
                             slot[RU1 * PLANE + x] * slot[U1 * PLANE + x] +
                             slot[RU2 * PLANE + x] * slot[U2 * PLANE + x]);
+    const double p = k.gm1 * e;
     slot[RHOE_F * PLANE + x] = e;
+    slot[PF * PLANE + x] = p;
+    slot[TF * PLANE + x] = k.gM2 * p / rho;
   }
+}
+
+// Epilogue of a fused stage: q = q_saved + coef*R and u = rhou/rho
+// (physics.py:192-194); p and T are left to the next stage's arrival
+// conversion (or a final primitives pass).
+__device__ __forceinline__ void stage_update(const double* sv, const double* R, double coef,
+                                             double* q) {
+#pragma unroll
+  for (int f = 0; f < 5; ++f) q[f] = sv[f] + coef * R[f];
+  q[U0] = q[RU0] / q[RHO];
+  q[U1] = q[RU1] / q[RHO];
+  q[U2] = q[RU2] / q[RHO];
 }
 
 // Centre-plane inner-derivative buffers (SN): D(u0,x0), D(u1,x1), D(u2,x2)
@@ -234,7 +258,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int64_t tile = p_seg / g.n0;
     const int plane = (int)(p_seg % g.n0) - 2 + p_r;
     const int slot = issued % NR;
-    mbar_expect_tx(&bars[slot], SLOT * 8);
+    mbar_expect_tx(&bars[slot], LOAD_BYTES);
     tma_load_plane(sm + slot * SLOT, &tin, &bars[slot], (int)(tile % ntk) * TK + g.h - 2,
                    (int)(tile / ntk) * TJ + g.h - 2, plane + g.h);
     ++issued;
@@ -268,7 +292,7 @@ __global__ void __launch_bounds__(NT, 1)
       const int first = t == 0 ? w : w + 4;
       for (int pp = first; pp <= w + 4; ++pp) {
         mbar_wait(&bars[pp % NR], (pp / NR) & 1);
-        to_internal_energy(sm + (pp % NR) * SLOT);
+        stage_arrival(k, sm + (pp % NR) * SLOT, tid, NT);
       }
       double* bufs = bufs0 + (w & 1) * NBUF * PLANE;
       if constexpr (kBuf) {
@@ -354,10 +378,8 @@ __global__ void __launch_bounds__(NT, 1)
           const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(jj + g.h) * g.s1 + (kk + g.h);
           double q[NFIELDS];
           (void)c;
-#pragma unroll
-          for (int f = 0; f < 5; ++f) q[f] = sv[f] + coef * R[f];
-          primitives_point(k, q, q + 5);
-          emit<NFIELDS>(out, g, i, jj, kk, q, wrap_mask);
+          stage_update(sv, R, coef, q);
+          emit<NOUT_STAGE>(out, g, i, jj, kk, q, wrap_mask);
         }
       }
     }
