@@ -89,10 +89,10 @@ int32_t fdns_stage(int32_t variant, const double* in, const double* saved,
                    const fdns_problem* pb, void* stream);
 
 /* Test hook selecting the kernel family: 0 = default (TMA-staged tiled
- * kernels where the row pitch allows; SN on two warp groups per point),
- * 1 = one-thread-per-point kernels (global-memory taps) for every variant,
- * 2 = default but SN on the single-group tiled kernel.  All paths are
- * parity-tested. */
+ * kernels where the row pitch allows), 1 = one-thread-per-point kernels
+ * (global-memory taps) for every variant, 3 = default but SN on two warp
+ * groups per point (experimental; slower on B200).  All
+ * paths are parity-tested. */
 void fdns_set_kernel_path(int32_t path);
 
 /* Test hook: force the persistent tiled kernels onto `ctas` CTAs (0 =

@@ -23,7 +23,7 @@ using namespace fdns;
 namespace {
 
 thread_local std::string g_err;
-int g_kernel_path = 0;        // test hook: 0 default, 1 point kernels, 2 single-group SN
+int g_kernel_path = 0;        // test hook: 0 default, 1 point kernels, 3 two-group SN
 int g_tiled_ctas = 0;         // test hook: force the tiled grid size (0 = one per SM)
 std::atomic<long long> g_launches{0};
 inline void count(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
@@ -490,8 +490,8 @@ int launch_residual(int variant, const double* in, const double* saved, double* 
       case FDNS_RA: launch_tiled_v<FDNS_RA, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
       case FDNS_RS: launch_tiled_v<FDNS_RS, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
       case FDNS_SN:
-        if (g_kernel_path == 2) launch_tiled_v<FDNS_SN, MODE>(m, saved, out, work, k, g, coef, wrap, s);
-        else launch_sn2<MODE>(m, saved, out, k, g, coef, wrap, s);
+        if (g_kernel_path == 3) launch_sn2<MODE>(m, saved, out, k, g, coef, wrap, s);
+        else launch_tiled_v<FDNS_SN, MODE>(m, saved, out, work, k, g, coef, wrap, s);
         break;
       case FDNS_SS: launch_tiled_v<FDNS_SS, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
       default: return fail("unknown variant");
