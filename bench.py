@@ -130,17 +130,21 @@ def cpu_cores() -> int:
     return len(os.sched_getaffinity(0))
 
 
-def run_cpu_oracle(n: int, steps: int, warmup: int = 1):
+def run_cpu_oracle(n: int, steps: int, warmup: int = 1, min_seconds: float = 0.0):
     """The C + OpenMP restatement of the reference path (oracle/), timed on
-    the host cores: pt-stage/s."""
+    the host cores: pt-stage/s.  Runs `steps` iterations, repeated until at
+    least `min_seconds` of CPU work has been timed."""
     from oracle import c_oracle, numpy_oracle as npo
     c = npo.Consts()
     F = npo.taylor_green(n, c)
     c_oracle.run(F, c, DT.get(n, 3.385e-3), warmup)
-    t0 = time.perf_counter()
-    c_oracle.run(F, c, DT.get(n, 3.385e-3), steps)
-    dt = time.perf_counter() - t0
-    return n ** 3 * 3 * steps / dt, dt
+    done, dt = 0, 0.0
+    while done == 0 or dt < min_seconds:
+        t0 = time.perf_counter()
+        c_oracle.run(F, c, DT.get(n, 3.385e-3), steps)
+        dt += time.perf_counter() - t0
+        done += steps
+    return n ** 3 * 3 * done / dt, dt, done
 
 
 # ------------------------------------------------------------------ ours
@@ -221,6 +225,59 @@ def bench_variant(fd, variant, grid, steps, warmup, flush_buf, lib):
     stage_ms = float(np.median([a.elapsed_time(b) for a, b in kev]))
     del graph
     return total_ms, launches, stage_ms
+
+
+def measured_traffic(variant: str, n: int):
+    """DRAM bytes per launch of the headline stage kernel from the committed
+    ncu --set full capture (profiles/traffic.json), if one matches."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    rec = json.load(open(path)).get(f"{variant}@{n}")
+    if not rec:
+        return None
+    return {"bytes_per_launch": rec["dram_bytes"], "unit": "B",
+            "bytes_per_point": rec["dram_bytes"] / n ** 3,
+            "source": rec["source"]}
+
+
+def stage_sweep(fd, lib, sizes, variants, flush, fp64_tf, hbm_peak):
+    """Steady-state view: one fused stage per variant at larger grids
+    (CUDA events, L2 flushed before each launch).  Informational; the
+    headline is the configs[1] workload above."""
+    import torch
+    from paper_1610_09146_b200 import _lib
+    c = fd.PhysicalConstants()
+    out = {}
+    for n in sizes:
+        g = fd.make_grid((n,) * 3, (2 * np.pi,) * 3)
+        s = fd.taylor_green_init(g, c)
+        for v in variants:
+            ev = fd.ResidualEvaluator(g, c, v)
+            Y, Z = ev.workspace()
+            ts = []
+            for r in range(5):
+                _lib.check(lib.fdns_l2_flush(_lib.ptr(flush), flush.numel(),
+                                             _lib.stream_handle()))
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record()
+                ev.stage(s.bundle, s.bundle, Y, 1e-30)
+                b.record()
+                torch.cuda.synchronize()
+                if r >= 2:
+                    ts.append(a.elapsed_time(b) / 1e3)
+            sec = float(np.median(ts))
+            pts = n ** 3 / sec
+            t_f = STAGE_FLOPS[v] / (fp64_tf * 1e12)
+            t_b = stage_bytes(v) / (hbm_peak * 1e9)
+            out[f"{v}@{n}"] = {"pt_stage_per_s": pts, "stage_ms": sec * 1e3,
+                               "frac_of_roofline": pts * max(t_f, t_b),
+                               "bound": "fp64" if t_f >= t_b else "hbm"}
+            del ev, Y, Z
+        del s
+        torch.cuda.empty_cache()
+    return out
 
 
 def fp64_peak(lib):
@@ -344,16 +401,21 @@ def main_ours(args):
                 "peak": hbm_peak, "unit": "GB/s",
                 "peak_source": f"{hbm_src} (MEASURED_PEAKS.json hbm_gbs)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof["traffic"] = measured_traffic(head, n)
     roof["kernel"] = f"fused stage ({head}): residual+RK update+primitives"
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        cpu_steps = max(1, args.cpu_steps)
-        v, sec = run_cpu_oracle(n, cpu_steps)
+        v, sec, done = run_cpu_oracle(n, max(1, args.cpu_steps),
+                                      min_seconds=args.cpu_seconds)
         cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
-               "sample": f"C+OpenMP oracle (SN route), TGV {n}^3, "
-                         f"{cpu_steps} RK3 steps after 1 warm-up, {sec:.1f} s"}
+               "sample": f"C+OpenMP oracle (SN route, pinned bitwise to the "
+                         f"reference), TGV {n}^3, {done} RK3 steps after 1 "
+                         f"warm-up, {sec:.1f} s"}
+    sizes = {}
+    if world == 1 and args.sizes:
+        sizes = stage_sweep(fd, lib, [int(x) for x in args.sizes.split(",")],
+                            args.variants, flush, fp64_tf, hbm_peak)
     e2e = bench_e2e(fd, head, grid, max(3, min(args.steps, 20))) \
         if world == 1 else None
 
@@ -374,6 +436,7 @@ def main_ours(args):
         "roofline": roof,
         "fp64_peak_tflops_measured": fp64_tf,
         "cpu_baseline": cpu,
+        "stage_sweep": sizes,
         "e2e": e2e,
         "gpu_launches": r["gpu_launches"],
         "clocks": clocks.summary(),
@@ -388,9 +451,8 @@ def main_reference(args):
         return
     n = args.n
     steps = max(1, min(args.steps, args.cpu_steps))
-    for _ in range(args.warmup and 1):
-        pass
-    val, sec = run_cpu_oracle(n, steps, warmup=1)
+    val, sec, steps = run_cpu_oracle(n, steps, warmup=1,
+                                     min_seconds=args.cpu_seconds)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
         "n_gpus": world, "steps": steps, "warmup": 1,
@@ -419,6 +481,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--cpu-steps", type=int, default=20)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="minimum timed CPU work for the baseline sample")
+    ap.add_argument("--sizes", default="128,256",
+                    help="extra grid sizes for the steady-state stage sweep")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.variants = [v.strip().upper() for v in args.variants.split(",")]

@@ -200,52 +200,62 @@ __global__ void __launch_bounds__(256) k_residual(const double* __restrict__ in,
   }
 }
 
-// BL fill: the 54 plain/product derivatives of every interior point into
-// their work arrays (plan.py:369-392; products formed per point, bitwise
-// equal to the scratch route).  The diagonal velocity gradients are written
-// by k_diag_ext over the extended region instead.
 template <int A_, int L>
-__device__ __forceinline__ void fill_axis(const Coef& k, const GAcc& a, double* __restrict__ wa,
-                                          int64_t fs) {
-  if constexpr (!(L >= S_U && L < S_U + 3 && (L - S_U) == A_))
-    wa[slot(A_, L) * fs + a.c] = eval_slot<A_, L>(k, a);
-  if constexpr (L + 1 < S_PER_AXIS) fill_axis<A_, L + 1>(k, a, wa, fs);
+__device__ __forceinline__ void fill_axis_all(const Coef& k, const GAcc& a,
+                                              double* __restrict__ wa, int64_t fs) {
+  wa[slot(A_, L) * fs + a.c] = eval_slot<A_, L>(k, a);
+  if constexpr (L + 1 < S_PER_AXIS) fill_axis_all<A_, L + 1>(k, a, wa, fs);
 }
 
-template <int A_>
-__global__ void __launch_bounds__(256) k_fill_bl(const double* __restrict__ in,
-                                                 double* __restrict__ wa, Coef k, Geom g) {
+// All 54 plain/product derivatives of an interior point in one pass over the
+// fields (the reference's separate fill loops, plan.py:369-392, fused; each
+// value is the same expression, so bitwise equal).
+__global__ void __launch_bounds__(256) k_fill_bl_all(const double* __restrict__ in,
+                                                     double* __restrict__ wa, Coef k, Geom g) {
   const int kk = blockIdx.x * blockDim.x + threadIdx.x;
   const int jj = blockIdx.y * blockDim.y + threadIdx.y;
   const int ii = blockIdx.z;
   if (kk >= g.n2 || jj >= g.n1) return;
   const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
   GAcc a{in, c, g.s0, g.s1, g.fs};
-  fill_axis<A_, 0>(k, a, wa, g.fs);
+  fill_axis_all<0, 0>(k, a, wa, g.fs);
+  fill_axis_all<1, 0>(k, a, wa, g.fs);
+  fill_axis_all<2, 0>(k, a, wa, g.fs);
 }
 
-// Diagonal velocity gradients D(u_q, x_q) on every point whose axis-q
-// coordinate is interior (other axes over the full padded range): exactly the
-// values the reference's halo-exchanged inner arrays hold (plan.py:378-379),
-// computed redundantly instead of exchanged, so slab ranks need no second
-// exchange.  dst[q] is the array for D(u_q, x_q).
-__global__ void k_diag_ext(const double* __restrict__ in, double* d0, double* d1p, double* d2p,
-                           Coef k, Geom g) {
+// D(u_Q, x_Q) on the ghost frame only: points whose axis-Q coordinate is
+// interior while another coordinate lies in the halo (the interior values
+// come from the fill kernels).  Together they hold exactly what the
+// reference's halo-exchanged inner arrays hold (plan.py:378-379).
+template <int Q>
+__global__ void k_diag_ghost(const double* __restrict__ in, double* __restrict__ dst, Coef k,
+                             Geom g) {
   const int h = g.h;
-  const int P1 = g.n1 + 2 * h, P2 = g.n2 + 2 * h;
-  const int64_t total = g.fs;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < total;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    const int kq = c % P2;
-    const int jq = (c / P2) % P1;
-    const int iq = c / g.s0;
-    const bool in0 = iq >= h && iq < g.n0 + h;
-    const bool in1 = jq >= h && jq < g.n1 + h;
-    const bool in2 = kq >= h && kq < g.n2 + h;
+  const int n[3] = {g.n0, g.n1, g.n2};
+  constexpr int A = Q == 0 ? 1 : 0;   // the two other axes, A < B
+  constexpr int B = Q == 2 ? 1 : 2;
+  const int PA = n[A] + 2 * h, PB = n[B] + 2 * h;
+  const int64_t frame = (int64_t)2 * h * PB + (int64_t)n[A] * 2 * h;
+  const int64_t total = frame * n[Q];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(t / frame) + h;
+    int64_t f = t % frame;
+    int ca, cb;
+    if (f < (int64_t)2 * h * PB) {            // ghost rows of axis A, all of B
+      ca = (int)(f / PB); cb = (int)(f % PB);
+      ca = ca < h ? ca : n[A] + ca;
+    } else {                                   // interior A, ghost columns of B
+      f -= (int64_t)2 * h * PB;
+      ca = (int)(f / (2 * h)) + h; cb = (int)(f % (2 * h));
+      cb = cb < h ? cb : n[B] + cb;
+    }
+    (void)PA;
+    int idx[3];
+    idx[Q] = q; idx[A] = ca; idx[B] = cb;
+    const int64_t c = idx[0] * g.s0 + idx[1] * g.s1 + idx[2];
     GAcc a{in, c, g.s0, g.s1, g.fs};
-    if (in0) d0[c] = d1<0, E_FIELD, U0, 0>(k, a);
-    if (in1) d1p[c] = d1<1, E_FIELD, U1, 0>(k, a);
-    if (in2) d2p[c] = d1<2, E_FIELD, U2, 0>(k, a);
+    dst[c] = d1<Q, E_FIELD, U0 + Q, 0>(k, a);
   }
 }
 
@@ -278,6 +288,9 @@ __global__ void __launch_bounds__(256) k_grad_ss(const double* __restrict__ in,
   if (kk >= g.n2 || jj >= g.n1) return;
   const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
   GAcc a{in, c, g.s0, g.s1, g.fs};
+  ws[(0 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U0, 0>(k, a);
+  ws[(1 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U1, 0>(k, a);
+  ws[(2 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U2, 0>(k, a);
   ws[(0 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U0, 0>(k, a);
   ws[(0 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U0, 0>(k, a);
   ws[(1 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U1, 0>(k, a);
@@ -518,23 +531,28 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
                  cudaStream_t s) {
   const dim3 blk(32, 8, 1);
   const dim3 grd = point_grid(g, blk);
-  const int ext_blocks = (int)std::min<int64_t>((g.fs + 255) / 256, 148 * 16);
+  auto ghosts = [&](double* d0, double* d1p, double* d2p) {
+    const int h = g.h;
+    const int64_t f0 = (int64_t)g.n0 * (2 * h * (g.n2 + 2 * h) + (int64_t)g.n1 * 2 * h);
+    const int64_t f1 = (int64_t)g.n1 * (2 * h * (g.n2 + 2 * h) + (int64_t)g.n0 * 2 * h);
+    const int64_t f2 = (int64_t)g.n2 * (2 * h * (g.n1 + 2 * h) + (int64_t)g.n0 * 2 * h);
+    auto nb = [](int64_t t) { return (int)std::min<int64_t>((t + 255) / 256, 148 * 8); };
+    k_diag_ghost<0><<<nb(f0), 256, 0, s>>>(in, d0, k, g);
+    k_diag_ghost<1><<<nb(f1), 256, 0, s>>>(in, d1p, k, g);
+    k_diag_ghost<2><<<nb(f2), 256, 0, s>>>(in, d2p, k, g);
+  };
   if (variant == FDNS_BL) {
-    k_fill_bl<0><<<grd, blk, 0, s>>>(in, work, k, g);
-    k_fill_bl<1><<<grd, blk, 0, s>>>(in, work, k, g);
-    k_fill_bl<2><<<grd, blk, 0, s>>>(in, work, k, g);
-    k_diag_ext<<<ext_blocks, 256, 0, s>>>(in, work + slot(0, S_U + 0) * g.fs,
-                                          work + slot(1, S_U + 1) * g.fs,
-                                          work + slot(2, S_U + 2) * g.fs, k, g);
+    k_fill_bl_all<<<grd, blk, 0, s>>>(in, work, k, g);
+    ghosts(work + slot(0, S_U + 0) * g.fs, work + slot(1, S_U + 1) * g.fs,
+           work + slot(2, S_U + 2) * g.fs);
     k_fill_cross<<<grd, blk, 0, s>>>(work, k, g);
     count(5);
     return check_launch("BL fills");
   }
   if (variant == FDNS_SS || variant == FDNS_RS) {
     k_grad_ss<<<grd, blk, 0, s>>>(in, work, k, g);
-    k_diag_ext<<<ext_blocks, 256, 0, s>>>(in, work + 0 * g.fs, work + 4 * g.fs, work + 8 * g.fs,
-                                          k, g);
-    count(2);
+    ghosts(work + 0 * g.fs, work + 4 * g.fs, work + 8 * g.fs);
+    count(4);
     return check_launch("SS fills");
   }
   return 0;
