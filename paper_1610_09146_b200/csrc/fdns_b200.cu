@@ -453,13 +453,13 @@ int num_sms() {
   return g_num_sms;
 }
 
-template <int V, int MODE>
+template <int V, int MODE, bool LAZY = true>
 int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const double* work,
                    const Coef& k, const Geom& g, double coef, int wrap, cudaStream_t s) {
   constexpr int smem = V == FDNS_SN ? tiled::SMEM_BYTES_SN : tiled::SMEM_BYTES;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tiled::k_stage_tiled<V, MODE>,
+    cudaFuncSetAttribute(tiled::k_stage_tiled<V, MODE, LAZY>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
@@ -469,7 +469,7 @@ int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const
   // one persistent CTA per SM, each at least ~4 plane steps
   int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(num_sms(), total / 4));
   if (g_tiled_ctas > 0) ctas = std::min<int64_t>(g_tiled_ctas, total);
-  tiled::k_stage_tiled<V, MODE><<<(unsigned)ctas, tiled::NT, smem, s>>>(
+  tiled::k_stage_tiled<V, MODE, LAZY><<<(unsigned)ctas, tiled::NT, smem, s>>>(
       m, work, saved, out, k, g, coef, ntk, total, wrap);
   return 0;
 }
@@ -504,6 +504,8 @@ int launch_residual(int variant, const double* in, const double* saved, double* 
       case FDNS_RS: launch_tiled_v<FDNS_RS, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
       case FDNS_SN:
         if (g_kernel_path == 3) launch_sn2<MODE>(m, saved, out, k, g, coef, wrap, s);
+        else if (g_kernel_path == 4)
+          launch_tiled_v<FDNS_SN, MODE, false>(m, saved, out, work, k, g, coef, wrap, s);
         else launch_tiled_v<FDNS_SN, MODE>(m, saved, out, work, k, g, coef, wrap, s);
         break;
       case FDNS_SS: launch_tiled_v<FDNS_SS, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;

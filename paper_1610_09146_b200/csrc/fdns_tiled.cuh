@@ -211,6 +211,43 @@ struct TiledLocalProvider {
   template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const { return v[S_DD + dd_index(J, O)]; }
 };
 
+// Lazily evaluated SN provider over the staged tile: a derivative is
+// evaluated where it is used (repeated uses merged by the compiler), the
+// diagonal velocity gradients and mixed terms come from the buffers/queues.
+struct TiledLazyProvider {
+  const Coef& k;
+  const SAcc& a;
+  const double* q1;   // D(u1,x1) at this column, planes i-2..i+2
+  const double* q2;   // D(u2,x2)
+  const double* b0;   // D(u0,x0) centre of the box buffer (pitch PK)
+  const double* b1;   // D(u1,x1) centre (pitch PK)
+  const double* b2;   // D(u2,x2) centre (pitch PK)
+  template <int A_, int L, int OCC = 0>
+  __device__ __forceinline__ double g() const {
+    if constexpr (L == S_U + A_) {
+      if constexpr (A_ == 0) return b0[0];
+      else if constexpr (A_ == 1) return q1[2];
+      else return q2[2];
+    } else {
+      return eval_slot<A_, L>(k, a);
+    }
+  }
+  template <int J, int O, int OCC = 0>
+  __device__ __forceinline__ double x() const {
+    if constexpr (O == 0) {
+      const double* q = J == 1 ? q1 : q2;
+      return k.w1[0] * (q[3] - q[1]) + k.w2[0] * (q[4] - q[0]);
+    } else if constexpr (J == 0) {
+      constexpr int s = O == 1 ? PK : 1;
+      return k.w1[O] * (b0[s] - b0[-s]) + k.w2[O] * (b0[2 * s] - b0[-2 * s]);
+    } else if constexpr (J == 2) {
+      return k.w1[1] * (b2[PK] - b2[-PK]) + k.w2[1] * (b2[2 * PK] - b2[-2 * PK]);
+    } else {
+      return k.w1[2] * (b1[1] - b1[-1]) + k.w2[2] * (b1[2] - b1[-2]);
+    }
+  }
+};
+
 // Static, balanced work split of one stage: the (tile, plane) steps in
 // tile-major order are cut into gridDim.x equal ranges; a CTA walks its
 // range as <= a few segments (one per tile touched).  The TMA producer
@@ -225,7 +262,7 @@ struct Segments {
   }
 };
 
-template <int V, int MODE>
+template <int V, int MODE, bool LAZY = true>
 __global__ void __launch_bounds__(NT, 1)
     k_stage_tiled(const __grid_constant__ CUtensorMap tin, const double* __restrict__ work,
                   const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
@@ -358,9 +395,15 @@ __global__ void __launch_bounds__(NT, 1)
       }
       double R[5];
       if constexpr (V == FDNS_SN) {
-        TiledLocalProvider P(k, a, q1, q2, bufs + toff, bufs + PLANE + toff,
-                             bufs + 2 * PLANE + toff);
-        residual_point<true>(k, P, r, R);
+        if constexpr (LAZY) {
+          const TiledLazyProvider P{k, a, q1, q2, bufs + toff, bufs + PLANE + toff,
+                                    bufs + 2 * PLANE + toff};
+          residual_point<true>(k, P, r, R);
+        } else {
+          TiledLocalProvider P(k, a, q1, q2, bufs + toff, bufs + PLANE + toff,
+                               bufs + 2 * PLANE + toff);
+          residual_point<true>(k, P, r, R);
+        }
       } else if constexpr (V == FDNS_RA) {
         InlineProvider<SAcc> P(k, a);
         residual_point<true>(k, P, r, R);
