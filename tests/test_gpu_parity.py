@@ -317,3 +317,57 @@ def test_sn_kernel_families_agree(kernel_path, ctas):
         finals.append(host_cons(st))
     for f in finals[1:]:
         assert np.array_equal(finals[0], f)
+
+
+# ------------------------------------------------ decomposition invariance
+@pytest.mark.parametrize("variant", ["SN", "SS", "BL", "RA"])
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_slab_decomposition_bitwise_invariant(variant, nranks):
+    """z-slab decomposition emulated on one GPU: each 'rank' owns
+    a slab grid (wrap_mask 0b110, so its stage kernels write axis-1/2 ghosts
+    only) and the axis-0 ghost planes are copied between the ranks' bundles
+    after every stage, as Slab.exchange does over NCCL.  The ranks' kernels
+    never wait on each other (the host sequences stage -> exchange), so this
+    is a faithful single-GPU emulation.  Fields must equal the one-GPU run
+    bitwise."""
+    n0, n1, n2, h = 24, 16, 20, 2
+    npts = (n0, n1, n2)
+    F = npo.manufactured(npts, CO)
+    g1 = grid_of(npts)
+    ref = state_from_cons(g1, npo.interior(F[:5], 2))
+    scheme = fd.RKScheme(dt=2e-3)
+    fd.run(ref, scheme, fd.ResidualEvaluator(g1, C, variant), 2)
+    want = host_cons(ref)
+
+    slabs = [fd.Slab.partition(n0, r, nranks) for r in range(nranks)]
+    grids, states, evs = [], [], []
+    for sl in slabs:
+        g = fd.make_grid(npts, (TWO_PI,) * 3, slab=sl)
+        st = fd.ConservativeState(g)
+        lo = sl.offset0
+        st.bundle[:5].copy_(torch.from_numpy(np.ascontiguousarray(
+            F[:5, lo:lo + sl.local_n0 + 2 * h])))
+        fd.eval_primitives_fused(st, C)        # over the padded slab
+        grids.append(g); states.append(st)
+        evs.append(fd.ResidualEvaluator(g, C, variant))
+
+    def exchange(bundles):
+        for r, sl in enumerate(slabs):
+            dn, up = slabs[r - 1], slabs[(r + 1) % nranks]
+            b, bd, bu = bundles[r], bundles[r - 1], bundles[(r + 1) % nranks]
+            n = sl.local_n0
+            b[:, 0:h].copy_(bd[:, dn.local_n0:dn.local_n0 + h])
+            b[:, n + h:n + 2 * h].copy_(bu[:, h:2 * h])
+
+    for _ in range(2):
+        X = [st.bundle for st in states]
+        YZ = [ev.workspace() for ev in evs]
+        src = [X, [y for y, _ in YZ], [z for _, z in YZ]]
+        dst = [src[1], src[2], X]
+        for k in range(3):
+            coef = scheme.alpha[k] * scheme.dt
+            for r in range(nranks):
+                evs[r].stage(src[k][r], X[r], dst[k][r], coef)
+            exchange(dst[k])
+    got = np.concatenate([host_cons(st) for st in states], axis=1)
+    assert np.array_equal(got, want)
