@@ -88,6 +88,17 @@ int32_t fdns_stage(int32_t variant, const double* in, const double* saved,
                    double* out, double* work, double coef, int32_t wrap_mask,
                    const fdns_problem* pb, void* stream);
 
+/* The fused stage restricted to local axis-0 planes [i_lo, i_hi) (interior
+ * indices); work-array fills over the whole slab first when with_fills.  A
+ * z-slab rank updates its 2h boundary planes, starts the halo exchange on a
+ * communication stream, and updates the interior planes meanwhile
+ * (decomp.py); the union of the ranges is bitwise fdns_stage. */
+int32_t fdns_stage_planes(int32_t variant, const double* in,
+                          const double* saved, double* out, double* work,
+                          double coef, int32_t wrap_mask, int32_t i_lo,
+                          int32_t i_hi, int32_t with_fills,
+                          const fdns_problem* pb, void* stream);
+
 /* Test hook selecting the kernel family: 0 = default (TMA-staged tiled
  * kernels where the row pitch allows), 1 = one-thread-per-point kernels
  * (global-memory taps) for every variant, 3 = default but SN on two warp

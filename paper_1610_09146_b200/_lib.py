@@ -51,6 +51,8 @@ EXPORTS = {
                             ctypes.POINTER(Problem), _VP]),
     "fdns_stage": (_I, [_I, _VP, _VP, _VP, _VP, ctypes.c_double, _I,
                         ctypes.POINTER(Problem), _VP]),
+    "fdns_stage_planes": (_I, [_I, _VP, _VP, _VP, _VP, ctypes.c_double, _I, _I,
+                               _I, _I, ctypes.POINTER(Problem), _VP]),
     "fdns_set_kernel_path": (None, [_I]),
     "fdns_set_tiled_grid": (None, [_I]),
     "fdns_diag_partials_size": (_I, [ctypes.POINTER(Problem)]),

@@ -159,10 +159,11 @@ template <int V, int MODE>
 __global__ void __launch_bounds__(256) k_residual(const double* __restrict__ in,
                                                   const double* saved, double* out,
                                                   const double* __restrict__ work, Coef k,
-                                                  Geom g, double coef, int wrap_mask) {
+                                                  Geom g, double coef, int wrap_mask,
+                                                  int i_lo) {
   const int kk = blockIdx.x * blockDim.x + threadIdx.x;
   const int jj = blockIdx.y * blockDim.y + threadIdx.y;
-  const int ii = blockIdx.z;
+  const int ii = blockIdx.z + i_lo;
   if (kk >= g.n2 || jj >= g.n1) return;
   const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
   double r[NFIELDS];
@@ -455,7 +456,8 @@ int num_sms() {
 
 template <int V, int MODE, bool LAZY = true>
 int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const double* work,
-                   const Coef& k, const Geom& g, double coef, int wrap, cudaStream_t s) {
+                   const Coef& k, const Geom& g, double coef, int wrap, int i_lo, int i_hi,
+                   cudaStream_t s) {
   constexpr int smem = V == FDNS_SN ? tiled::SMEM_BYTES_SN : tiled::SMEM_BYTES;
   static bool attr = false;
   if (!attr) {
@@ -465,18 +467,19 @@ int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const
   }
   const int ntk = (g.n2 + tiled::TK - 1) / tiled::TK;
   const int ntj = (g.n1 + tiled::TJ - 1) / tiled::TJ;
-  const int64_t total = (int64_t)ntk * ntj * g.n0;
+  const int nplanes = i_hi - i_lo;
+  const int64_t total = (int64_t)ntk * ntj * nplanes;
   // one persistent CTA per SM, each at least ~4 plane steps
   int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(num_sms(), total / 4));
   if (g_tiled_ctas > 0) ctas = std::min<int64_t>(g_tiled_ctas, total);
   tiled::k_stage_tiled<V, MODE, LAZY><<<(unsigned)ctas, tiled::NT, smem, s>>>(
-      m, work, saved, out, k, g, coef, ntk, total, wrap);
+      m, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes);
   return 0;
 }
 
 template <int MODE>
 int launch_sn2(const CUtensorMap& m, const double* saved, double* out, const Coef& k,
-               const Geom& g, double coef, int wrap, cudaStream_t s) {
+               const Geom& g, double coef, int wrap, int i_lo, int i_hi, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(sn2::k_stage_sn2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -485,43 +488,46 @@ int launch_sn2(const CUtensorMap& m, const double* saved, double* out, const Coe
   }
   const int ntk = (g.n2 + tiled::TK - 1) / tiled::TK;
   const int ntj = (g.n1 + tiled::TJ - 1) / tiled::TJ;
-  const int64_t total = (int64_t)ntk * ntj * g.n0;
+  const int nplanes = i_hi - i_lo;
+  const int64_t total = (int64_t)ntk * ntj * nplanes;
   int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(num_sms(), total / 4));
   if (g_tiled_ctas > 0) ctas = std::min<int64_t>(g_tiled_ctas, total);
-  sn2::k_stage_sn2<MODE><<<(unsigned)ctas, sn2::NT, sn2::SMEM_BYTES, s>>>(m, saved, out, k, g, coef,
-                                                                          ntk, total, wrap);
+  sn2::k_stage_sn2<MODE><<<(unsigned)ctas, sn2::NT, sn2::SMEM_BYTES, s>>>(
+      m, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes);
   return 0;
 }
 
 template <int MODE>
 int launch_residual(int variant, const double* in, const double* saved, double* out,
                     double* work, const Coef& k, const Geom& g, double coef, int wrap,
-                    cudaStream_t s) {
+                    int i_lo, int i_hi, cudaStream_t s) {
+  if (i_hi <= i_lo) return 0;
   CUtensorMap m;
   if (variant != FDNS_BL && g_kernel_path != 1 && plane_map(&m, in, g)) {
     switch (variant) {
-      case FDNS_RA: launch_tiled_v<FDNS_RA, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
-      case FDNS_RS: launch_tiled_v<FDNS_RS, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
+      case FDNS_RA: launch_tiled_v<FDNS_RA, MODE>(m, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
+      case FDNS_RS: launch_tiled_v<FDNS_RS, MODE>(m, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
       case FDNS_SN:
-        if (g_kernel_path == 3) launch_sn2<MODE>(m, saved, out, k, g, coef, wrap, s);
+        if (g_kernel_path == 3) launch_sn2<MODE>(m, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
         else if (g_kernel_path == 4)
-          launch_tiled_v<FDNS_SN, MODE, false>(m, saved, out, work, k, g, coef, wrap, s);
-        else launch_tiled_v<FDNS_SN, MODE>(m, saved, out, work, k, g, coef, wrap, s);
+          launch_tiled_v<FDNS_SN, MODE, false>(m, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
+        else launch_tiled_v<FDNS_SN, MODE>(m, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
         break;
-      case FDNS_SS: launch_tiled_v<FDNS_SS, MODE>(m, saved, out, work, k, g, coef, wrap, s); break;
+      case FDNS_SS: launch_tiled_v<FDNS_SS, MODE>(m, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
       default: return fail("unknown variant");
     }
     count();
     return check_launch("tiled stage kernel");
   }
   const dim3 blk(32, 8, 1);
-  const dim3 grd = point_grid(g, blk);
+  dim3 grd = point_grid(g, blk);
+  grd.z = i_hi - i_lo;
   switch (variant) {
-    case FDNS_BL: k_residual<FDNS_BL, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap); break;
-    case FDNS_RA: k_residual<FDNS_RA, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap); break;
-    case FDNS_RS: k_residual<FDNS_RS, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap); break;
-    case FDNS_SN: k_residual<FDNS_SN, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap); break;
-    case FDNS_SS: k_residual<FDNS_SS, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap); break;
+    case FDNS_BL: k_residual<FDNS_BL, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap, i_lo); break;
+    case FDNS_RA: k_residual<FDNS_RA, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap, i_lo); break;
+    case FDNS_RS: k_residual<FDNS_RS, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap, i_lo); break;
+    case FDNS_SN: k_residual<FDNS_SN, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap, i_lo); break;
+    case FDNS_SS: k_residual<FDNS_SS, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap, i_lo); break;
     default: return fail("unknown variant");
   }
   count();
@@ -627,7 +633,7 @@ int32_t fdns_residual(int32_t variant, const double* state, double* work, double
   const Coef k = make_coef(pb);
   cudaStream_t s = (cudaStream_t)stream;
   if (int e = launch_fills(variant, state, work, k, g, s)) return e;
-  return launch_residual<0>(variant, state, nullptr, out, work, k, g, 0.0, 0, s);
+  return launch_residual<0>(variant, state, nullptr, out, work, k, g, 0.0, 0, 0, g.n0, s);
 }
 
 int32_t fdns_rk_update(double* cons, const double* saved, const double* res, double coef,
@@ -640,19 +646,30 @@ int32_t fdns_rk_update(double* cons, const double* saved, const double* res, dou
   return check_launch("rk update kernel");
 }
 
-int32_t fdns_stage(int32_t variant, const double* in, const double* saved, double* out,
-                   double* work, double coef, int32_t wrap_mask, const fdns_problem* pb,
-                   void* stream) {
+int32_t fdns_stage_planes(int32_t variant, const double* in, const double* saved, double* out,
+                          double* work, double coef, int32_t wrap_mask, int32_t i_lo,
+                          int32_t i_hi, int32_t with_fills, const fdns_problem* pb,
+                          void* stream) {
   if (int e = validate(pb)) return e;
   const int nw = fdns_workarray_count(variant);
   if (nw < 0) return fail("unknown variant");
   if (nw > 0 && !work) return fail("variant needs work arrays");
   if (in == out) return fail("fused stage needs distinct in/out bundles");
+  if (i_lo < 0 || i_hi > pb->n[0] || i_lo > i_hi) return fail("plane range outside the slab");
   const Geom g = make_geom(pb);
   const Coef k = make_coef(pb);
   cudaStream_t s = (cudaStream_t)stream;
-  if (int e = launch_fills(variant, in, work, k, g, s)) return e;
-  return launch_residual<1>(variant, in, saved, out, work, k, g, coef, wrap_mask, s);
+  if (with_fills)
+    if (int e = launch_fills(variant, in, work, k, g, s)) return e;
+  return launch_residual<1>(variant, in, saved, out, work, k, g, coef, wrap_mask, i_lo, i_hi, s);
+}
+
+int32_t fdns_stage(int32_t variant, const double* in, const double* saved, double* out,
+                   double* work, double coef, int32_t wrap_mask, const fdns_problem* pb,
+                   void* stream) {
+  if (int e = validate(pb)) return e;
+  return fdns_stage_planes(variant, in, saved, out, work, coef, wrap_mask, 0, pb->n[0], 1, pb,
+                           stream);
 }
 
 int32_t fdns_diag_partials_size(const fdns_problem*) { return DIAG_BLOCKS * DIAG_Q; }

@@ -83,7 +83,8 @@ struct LazyProvider {
 template <int MODE>
 __global__ void __launch_bounds__(NT, 1)
     k_stage_sn2(const __grid_constant__ CUtensorMap tin, const double* saved, double* out,
-                Coef k, Geom g, double coef, int ntk, int64_t total_steps, int wrap_mask) {
+                Coef k, Geom g, double coef, int ntk, int64_t total_steps, int wrap_mask,
+                int i_lo, int nplanes) {
   extern __shared__ __align__(128) double sm[];
   double* bset0 = sm + NR * SLOT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(bset0 + 2 * BSET);
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(NT, 1)
   const int pt = groupB ? tid - NPT : tid;
   const int tk = pt % TK, tj = pt / TK;
   tiled::Segments S{blockIdx.x * total_steps / gridDim.x,
-                    (blockIdx.x + 1) * total_steps / gridDim.x, g.n0};
+                    (blockIdx.x + 1) * total_steps / gridDim.x, nplanes};
   if (S.beg >= S.end) return;
 
   if (tid == 0) {
@@ -107,8 +108,8 @@ __global__ void __launch_bounds__(NT, 1)
   auto issue_next = [&]() {
     const int64_t se = S.seg_end(p_seg);
     const int len = (int)(se - p_seg) + 4;
-    const int64_t tile = p_seg / g.n0;
-    const int plane = (int)(p_seg % g.n0) - 2 + p_r;
+    const int64_t tile = p_seg / nplanes;
+    const int plane = i_lo + (int)(p_seg % nplanes) - 2 + p_r;
     const int slot = issued % NR;
     tiled::mbar_expect_tx(&bars[slot], tiled::LOAD_BYTES);
     tiled::tma_load_plane(sm + slot * SLOT, &tin, &bars[slot], (int)(tile % ntk) * TK + g.h - 2,
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(NT, 1)
   int w = 0;
   for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) {
     const int64_t se = S.seg_end(x);
-    const int64_t tile = x / g.n0;
+    const int64_t tile = x / nplanes;
     const int k0 = (int)(tile % ntk) * TK, j0 = (int)(tile / ntk) * TJ;
     const int jj = j0 + tj, kk = k0 + tk;
     const bool active = jj < g.n1 && kk < g.n2;
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(NT, 1)
       double r[NFIELDS];
 #pragma unroll
       for (int f = 0; f < NFIELDS; ++f) r[f] = a.v(f, 0, 0, 0);   // r[RHOE_F] = rho*e
-      const int i = (int)(x % g.n0) + t;
+      const int i = i_lo + (int)(x % nplanes) + t;
       const LazyProvider P{k, a, q1, q2, bs + toff, bs + B0_N + tj * PK + tk + 2,
                            bs + B0_N + B1_N + (tj + 2) * TK + tk};
       const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(min(jj, g.n1 - 1) + g.h) * g.s1 +

@@ -254,8 +254,8 @@ struct TiledLazyProvider {
 // (thread 0) streams the planes of all segments back to back through the
 // ring, prefetching across segment boundaries.
 struct Segments {
-  int64_t beg, end;   // [beg, end) in tile-major (tile * n0 + plane) order
-  int n0;
+  int64_t beg, end;   // [beg, end) in tile-major (tile * nplanes + plane) order
+  int n0;             // planes per tile in this launch
   __device__ __forceinline__ int64_t seg_end(int64_t x) const {
     const int64_t tile_end = (x / n0 + 1) * (int64_t)n0;
     return tile_end < end ? tile_end : end;
@@ -266,7 +266,7 @@ template <int V, int MODE, bool LAZY = true>
 __global__ void __launch_bounds__(NT, 1)
     k_stage_tiled(const __grid_constant__ CUtensorMap tin, const double* __restrict__ work,
                   const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
-                  int64_t total_steps, int wrap_mask) {
+                  int64_t total_steps, int wrap_mask, int i_lo, int nplanes) {
   extern __shared__ __align__(128) double sm[];
   constexpr bool kBuf = (V == FDNS_SN);
   double* bufs0 = sm + NR * SLOT;   // 2 x NBUF planes (SN only)
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(NT, 1)
   const int tid = threadIdx.x;
   const int tk = tid % TK, tj = tid / TK;
   Segments S{blockIdx.x * total_steps / gridDim.x, (blockIdx.x + 1) * total_steps / gridDim.x,
-             g.n0};
+             nplanes};
   if (S.beg >= S.end) return;
 
   if (tid == 0) {
@@ -292,8 +292,8 @@ __global__ void __launch_bounds__(NT, 1)
   auto issue_next = [&]() {
     const int64_t se = S.seg_end(p_seg);
     const int len = (int)(se - p_seg) + 4;
-    const int64_t tile = p_seg / g.n0;
-    const int plane = (int)(p_seg % g.n0) - 2 + p_r;
+    const int64_t tile = p_seg / nplanes;
+    const int plane = i_lo + (int)(p_seg % nplanes) - 2 + p_r;
     const int slot = issued % NR;
     mbar_expect_tx(&bars[slot], LOAD_BYTES);
     tma_load_plane(sm + slot * SLOT, &tin, &bars[slot], (int)(tile % ntk) * TK + g.h - 2,
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(NT, 1)
   int w = 0;   // stream position of the current window start
   for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) {
     const int64_t se = S.seg_end(x);
-    const int64_t tile = x / g.n0;
+    const int64_t tile = x / nplanes;
     const int k0 = (int)(tile % ntk) * TK, j0 = (int)(tile / ntk) * TJ;
     const int jj = j0 + tj, kk = k0 + tk;
     const bool active = jj < g.n1 && kk < g.n2;
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(NT, 1)
       double r[NFIELDS];
 #pragma unroll
       for (int f = 0; f < NFIELDS; ++f) r[f] = a.v(f, 0, 0, 0);   // r[RHOE_F] = rho*e
-      const int i = (int)(x % g.n0) + t;
+      const int i = i_lo + (int)(x % nplanes) + t;
       // issue the saved-state loads now; they land while the residual runs
       double sv[5];
       if constexpr (MODE == 1) {

@@ -166,6 +166,40 @@ class ResidualEvaluator:
             _lib.stream_handle()), f"stage ({self.plan.name})")
 
 
+    def stage_planes(self, inp: torch.Tensor, saved: torch.Tensor,
+                     out: torch.Tensor, coef: float, i_lo: int, i_hi: int,
+                     with_fills: bool) -> None:
+        """The fused stage on local axis-0 planes [i_lo, i_hi) only."""
+        _lib.check(self.lib.fdns_stage_planes(
+            self.plan.variant_id, _lib.ptr(inp), _lib.ptr(saved),
+            _lib.ptr(out), self.work_ptr, coef, self.wrap_mask, i_lo, i_hi,
+            int(with_fills), self.problem, _lib.stream_handle()),
+            f"stage ({self.plan.name})")
+
+    def stage_exchanged(self, inp: torch.Tensor, saved: torch.Tensor,
+                        out: torch.Tensor, coef: float) -> None:
+        """One stage of a z-slab rank with the halo exchange overlapped:
+        the 2h boundary planes are updated first, their exchange runs on a
+        communication stream while the interior planes are updated, and the
+        launching stream then waits for the exchange."""
+        slab, h = self.grid.slab, self.grid.halo
+        n = self.grid.local_npoints[0]
+        if n < 2 * h:
+            self.stage(inp, saved, out, coef)
+            slab.exchange(out, h)
+            return
+        main = torch.cuda.current_stream()
+        if getattr(self, "_comm", None) is None:
+            self._comm = torch.cuda.Stream()
+        self.stage_planes(inp, saved, out, coef, 0, h, True)
+        self.stage_planes(inp, saved, out, coef, n - h, n, False)
+        self._comm.wait_stream(main)
+        with torch.cuda.stream(self._comm):
+            slab.exchange(out, h)
+        self.stage_planes(inp, saved, out, coef, h, n - h, False)
+        main.wait_stream(self._comm)
+
+
 def assemble_residual(state: ConservativeState, constants: PhysicalConstants,
                       plan: KernelPlan | str, spec=None,
                       workers: int = 1) -> Residual:

@@ -322,7 +322,8 @@ def test_sn_kernel_families_agree(kernel_path, ctas):
 # ------------------------------------------------ decomposition invariance
 @pytest.mark.parametrize("variant", ["SN", "SS", "BL", "RA"])
 @pytest.mark.parametrize("nranks", [2, 3])
-def test_slab_decomposition_bitwise_invariant(variant, nranks):
+@pytest.mark.parametrize("split", [False, True])
+def test_slab_decomposition_bitwise_invariant(variant, nranks, split):
     """z-slab decomposition emulated on one GPU: each 'rank' owns
     a slab grid (wrap_mask 0b110, so its stage kernels write axis-1/2 ghosts
     only) and the axis-0 ghost planes are copied between the ranks' bundles
@@ -366,8 +367,18 @@ def test_slab_decomposition_bitwise_invariant(variant, nranks):
         dst = [src[1], src[2], X]
         for k in range(3):
             coef = scheme.alpha[k] * scheme.dt
-            for r in range(nranks):
-                evs[r].stage(src[k][r], X[r], dst[k][r], coef)
-            exchange(dst[k])
+            if split:   # the overlapped order of ResidualEvaluator.stage_exchanged
+                for r in range(nranks):
+                    n = slabs[r].local_n0
+                    evs[r].stage_planes(src[k][r], X[r], dst[k][r], coef, 0, h, True)
+                    evs[r].stage_planes(src[k][r], X[r], dst[k][r], coef, n - h, n, False)
+                exchange(dst[k])
+                for r in range(nranks):
+                    n = slabs[r].local_n0
+                    evs[r].stage_planes(src[k][r], X[r], dst[k][r], coef, h, n - h, False)
+            else:
+                for r in range(nranks):
+                    evs[r].stage(src[k][r], X[r], dst[k][r], coef)
+                exchange(dst[k])
     got = np.concatenate([host_cons(st) for st in states], axis=1)
     assert np.array_equal(got, want)
