@@ -139,6 +139,7 @@ __device__ __forceinline__ void emit(double* out, const Geom& g, int i, int j, i
 // intermediate the reference forms), T = (gM2*p)/rho.  Bitwise the values
 // the primitives pass would have stored.
 __device__ __forceinline__ void stage_arrival(const Coef& k, double* slot, int tid, int nthreads) {
+#pragma unroll 1
   for (int x = tid; x < PLANE; x += nthreads) {
     const double rho = slot[RHO * PLANE + x];
     const double e = slot[RHOE_F * PLANE + x] -
@@ -176,6 +177,8 @@ constexpr int BU2_N = PJ * TK;          // D(u2,x2): all rows, interior columns
 constexpr int BUF_WORK = PLANE + BU1_N + BU2_N;
 constexpr int SMEM_BYTES_SN = NR * SLOT * 8 + 2 * NBUF * PLANE * 8 + 128;
 static_assert(SMEM_BYTES_SN <= 232448, "SN tile exceeds the 227 KB shared-memory limit");
+static_assert(PLANE <= 2 * NT && BU1_N <= 2 * NT && BU2_N <= 2 * NT,
+              "centre-plane buffer items: at most two per thread");
 
 // SN provider over the staged tile: every distinct derivative once (LOCAL),
 // diagonal velocity gradients and the six mixed terms from the axis-0
@@ -334,20 +337,35 @@ __global__ void __launch_bounds__(NT, 1)
       double* bufs = bufs0 + (w & 1) * NBUF * PLANE;
       if constexpr (kBuf) {
         // centre-plane buffers over the staged box (u0..u2 are untouched by
-        // the energy conversion, so no barrier is needed before this)
-        for (int xx = tid; xx < BUF_WORK; xx += NT) {
-          int pos, which;
-          if (xx < PLANE) { pos = xx; which = 0; }
-          else if (xx < PLANE + BU1_N) { pos = 2 * PK + (xx - PLANE); which = 1; }
-          else { const int y = xx - PLANE - BU1_N; pos = (y / TK) * PK + 2 + y % TK; which = 2; }
-          SAcc b;
+        // the energy conversion, so no barrier is needed before this).
+        // Fixed per-thread items (no index math or branching per step): box
+        // positions tid and tid+NT of each buffer, predicated.
+        const double* base[5];
 #pragma unroll
-          for (int d = 0; d < 5; ++d) b.p[d] = sm + ((w + d) % NR) * SLOT + pos;
-          double val;
-          if (which == 0) val = d1<0, E_FIELD, U0, 0>(k, b);
-          else if (which == 1) val = d1<1, E_FIELD, U1, 0>(k, b);
-          else val = d1<2, E_FIELD, U2, 0>(k, b);
-          bufs[which * PLANE + pos] = val;
+        for (int d = 0; d < 5; ++d) base[d] = sm + ((w + d) % NR) * SLOT;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const int x0 = tid + m * NT;                       // D(u0,x0), whole box
+          if (m == 0 || x0 < PLANE) {
+            SAcc b;
+#pragma unroll
+            for (int d = 0; d < 5; ++d) b.p[d] = base[d] + x0;
+            bufs[x0] = d1<0, E_FIELD, U0, 0>(k, b);
+          }
+          const int y1 = tid + m * NT;                       // D(u1,x1), rows 2..TJ+1
+          if (y1 < BU1_N) {
+            const int pos = 2 * PK + y1;
+            SAcc b;
+            b.p[2] = base[2] + pos;
+            bufs[PLANE + pos] = d1<1, E_FIELD, U1, 0>(k, b);
+          }
+          const int y2 = tid + m * NT;                       // D(u2,x2), cols 2..TK+1
+          if (y2 < BU2_N) {
+            const int pos = (y2 / TK) * PK + 2 + y2 % TK;
+            SAcc b;
+            b.p[2] = base[2] + pos;
+            bufs[2 * PLANE + pos] = d1<2, E_FIELD, U2, 0>(k, b);
+          }
         }
       }
       __syncthreads();
