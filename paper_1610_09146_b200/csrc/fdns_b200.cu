@@ -211,7 +211,7 @@ __device__ __forceinline__ void fill_axis_all(const Coef& k, const GAcc& a,
 // All 54 plain/product derivatives of an interior point in one pass over the
 // fields (the reference's separate fill loops, plan.py:369-392, fused; each
 // value is the same expression, so bitwise equal).
-__global__ void __launch_bounds__(256) k_fill_bl_all(const double* __restrict__ in,
+__global__ void __launch_bounds__(256, 4) k_fill_bl_all(const double* __restrict__ in,
                                                      double* __restrict__ wa, Coef k, Geom g) {
   const int kk = blockIdx.x * blockDim.x + threadIdx.x;
   const int jj = blockIdx.y * blockDim.y + threadIdx.y;
@@ -261,7 +261,7 @@ __global__ void k_diag_ghost(const double* __restrict__ in, double* __restrict__
 }
 
 // BL mixed fills: outer derivative of the stored inner arrays (plan.py:380-382).
-__global__ void __launch_bounds__(256) k_fill_cross(double* __restrict__ wa, Coef k, Geom g) {
+__global__ void __launch_bounds__(256, 4) k_fill_cross(double* __restrict__ wa, Coef k, Geom g) {
   const int kk = blockIdx.x * blockDim.x + threadIdx.x;
   const int jj = blockIdx.y * blockDim.y + threadIdx.y;
   const int ii = blockIdx.z;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(256) k_fill_cross(double* __restrict__ wa, Coe
 
 // SS/RS fill: the six off-diagonal velocity gradients on the interior
 // (diagonals come from k_diag_ext).  ws[q*3+a] = D(u_q, x_a).
-__global__ void __launch_bounds__(256) k_grad_ss(const double* __restrict__ in,
+__global__ void __launch_bounds__(256, 4) k_grad_ss(const double* __restrict__ in,
                                                  double* __restrict__ ws, Coef k, Geom g) {
   const int kk = blockIdx.x * blockDim.x + threadIdx.x;
   const int jj = blockIdx.y * blockDim.y + threadIdx.y;

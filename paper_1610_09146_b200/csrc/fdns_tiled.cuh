@@ -214,52 +214,6 @@ struct TiledLocalProvider {
   template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const { return v[S_DD + dd_index(J, O)]; }
 };
 
-// SS / RS provider over the staged tile with the FETCHed values loaded up
-// front: the nine velocity gradients at the point and the four shifted
-// inner-derivative values of each mixed term (the stored arrays the
-// reference reads, codegen.py:111-113, plan.py:378-379) are issued as
-// global loads at the start of the plane step, so their latency overlaps the
-// LOCAL (SS) or INLINE (RS) derivative work.
-template <bool INLINE_REST>
-struct SSPrefetchProvider {
-  const Coef& k;
-  const SAcc& a;
-  double gv[9];     // D(u_q, x_a) at the point, [q*3+a]
-  double xs[6][4];  // inner D(u_J,x_J) at outer offsets +1, -1, +2, -2
-  __device__ __forceinline__ SSPrefetchProvider(const Coef& k_, const SAcc& a_,
-                                                const double* __restrict__ ws, int64_t c,
-                                                int64_t fs, int64_t s0, int64_t s1)
-      : k(k_), a(a_) {
-#pragma unroll
-    for (int m = 0; m < 9; ++m) gv[m] = __ldg(ws + m * fs + c);
-    const int64_t st[3] = {s0, s1, 1};
-#pragma unroll
-    for (int J = 0; J < 3; ++J) {
-      const double* inner = ws + (J * 3 + J) * fs + c;
-#pragma unroll
-      for (int O = 0; O < 3; ++O) {
-        if (O == J) continue;
-        const int x = dd_index(J, O);
-        xs[x][0] = __ldg(inner + st[O]);
-        xs[x][1] = __ldg(inner - st[O]);
-        xs[x][2] = __ldg(inner + 2 * st[O]);
-        xs[x][3] = __ldg(inner - 2 * st[O]);
-      }
-    }
-  }
-  template <int A_, int L, int OCC = 0>
-  __device__ __forceinline__ double g() const {
-    if constexpr (L >= S_U && L < S_U + 3) return gv[(L - S_U) * 3 + A_];
-    else if constexpr (INLINE_REST) return eval_slot<A_, L>(k, a.rebased(zero_offset<OCC>()));
-    else return eval_slot<A_, L>(k, a);
-  }
-  template <int J, int O, int OCC = 0>
-  __device__ __forceinline__ double x() const {
-    const double* v = xs[dd_index(J, O)];
-    return k.w1[O] * (v[0] - v[1]) + k.w2[O] * (v[2] - v[3]);
-  }
-};
-
 // Lazily evaluated SN provider over the staged tile: a derivative is
 // evaluated where it is used (repeated uses merged by the compiler), the
 // diagonal velocity gradients and mixed terms come from the buffers/queues.
@@ -475,7 +429,7 @@ __global__ void __launch_bounds__(NT, 1)
         // inactive (edge) threads read a valid clamped column; never written
         const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(min(jj, g.n1 - 1) + g.h) * g.s1 +
                           (min(kk, g.n2 - 1) + g.h);
-        SSPrefetchProvider<V == FDNS_RS> P(k, a, work, c, g.fs, g.s0, g.s1);
+        SSProvider<SAcc, V == FDNS_RS> P(k, a, work, c, g.fs, g.s0, g.s1);
         residual_point<true>(k, P, r, R);
       }
       if (active) {
