@@ -211,7 +211,7 @@ __device__ __forceinline__ void fill_axis_all(const Coef& k, const GAcc& a,
 // All 54 plain/product derivatives of an interior point in one pass over the
 // fields (the reference's separate fill loops, plan.py:369-392, fused; each
 // value is the same expression, so bitwise equal).
-__global__ void __launch_bounds__(256, 4) k_fill_bl_all(const double* __restrict__ in,
+__global__ void __launch_bounds__(256) k_fill_bl_all(const double* __restrict__ in,
                                                      double* __restrict__ wa, Coef k, Geom g) {
   const int kk = blockIdx.x * blockDim.x + threadIdx.x;
   const int jj = blockIdx.y * blockDim.y + threadIdx.y;
@@ -550,7 +550,11 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
     k_diag_ghost<2><<<nb(f2), 256, 0, s>>>(in, d2p, k, g);
   };
   if (variant == FDNS_BL) {
-    k_fill_bl_all<<<grd, blk, 0, s>>>(in, work, k, g);
+    CUtensorMap m;
+    if (g_kernel_path != 1 && plane_map(&m, in, g))
+      launch_tiled_v<FDNS_BL, 2>(m, nullptr, nullptr, work, k, g, 0.0, 0, 0, g.n0, s);
+    else
+      k_fill_bl_all<<<grd, blk, 0, s>>>(in, work, k, g);
     ghosts(work + slot(0, S_U + 0) * g.fs, work + slot(1, S_U + 1) * g.fs,
            work + slot(2, S_U + 2) * g.fs);
     k_fill_cross<<<grd, blk, 0, s>>>(work, k, g);

@@ -251,6 +251,15 @@ struct TiledLazyProvider {
   }
 };
 
+// BL work-array fill from the staged tile: the 54 plain/product derivatives
+// of one point into their arrays (plan.py:369-392).
+template <int A_, int L>
+__device__ __forceinline__ void fill_slots(const Coef& k, const SAcc& a, double* __restrict__ wa,
+                                           int64_t c, int64_t fs) {
+  wa[slot(A_, L) * fs + c] = eval_slot<A_, L>(k, a);
+  if constexpr (L + 1 < S_PER_AXIS) fill_slots<A_, L + 1>(k, a, wa, c, fs);
+}
+
 // Static, balanced work split of one stage: the (tile, plane) steps in
 // tile-major order are cut into gridDim.x equal ranges; a CTA walks its
 // range as <= a few segments (one per tile touched).  The TMA producer
@@ -399,10 +408,20 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
 
+      const int i = i_lo + (int)(x % nplanes) + t;
+      if constexpr (MODE == 2) {   // BL fill: derivative arrays only
+        if (active) {
+          const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(jj + g.h) * g.s1 + (kk + g.h);
+          double* wa = const_cast<double*>(work);
+          fill_slots<0, 0>(k, a, wa, c, g.fs);
+          fill_slots<1, 0>(k, a, wa, c, g.fs);
+          fill_slots<2, 0>(k, a, wa, c, g.fs);
+        }
+        continue;
+      }
       double r[NFIELDS];
 #pragma unroll
       for (int f = 0; f < NFIELDS; ++f) r[f] = a.v(f, 0, 0, 0);   // r[RHOE_F] = rho*e
-      const int i = i_lo + (int)(x % nplanes) + t;
       // issue the saved-state loads now; they land while the residual runs
       double sv[5];
       if constexpr (MODE == 1) {
