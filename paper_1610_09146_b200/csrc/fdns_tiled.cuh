@@ -99,8 +99,8 @@ struct SAcc {
 // of wrap_mask (mesh.py:118-139 semantics: ghost = value at the wrapped
 // coordinates).
 template <int NOUT>
-__device__ __forceinline__ void emit_ghosts(double* out, const Geom& g, int i, int j, int k,
-                                         const double* val, int wrap_mask) {
+__device__ __forceinline__ void emit(double* out, const Geom& g, int i, int j, int k,
+                                     const double* val, int wrap_mask) {
   const int h = g.h;
   int ci[3], cj[3], ck[3], ni = 1, nj = 1, nk = 1;
   ci[0] = i + h; cj[0] = j + h; ck[0] = k + h;
@@ -116,31 +116,21 @@ __device__ __forceinline__ void emit_ghosts(double* out, const Geom& g, int i, i
     if (k < h) ck[nk++] = k + h + g.n2;
     if (k >= g.n2 - h) ck[nk++] = k + h - g.n2;
   }
-  for (int a = 0; a < ni; ++a)
-    for (int b = 0; b < nj; ++b)
-      for (int d = 0; d < nk; ++d) {
-        if ((a | b | d) == 0) continue;
-        const int64_t c = ci[a] * g.s0 + cj[b] * g.s1 + ck[d];
+  {
+    const int64_t c = ci[0] * g.s0 + cj[0] * g.s1 + ck[0];
 #pragma unroll
-        for (int f = 0; f < NOUT; ++f) out[f * g.fs + c] = val[f];
-      }
-}
-
-// Write the NOUT output values of interior point (i, j, k) to its location
-// and to every periodic ghost image on the axes of wrap_mask (mesh.py:118-139
-// semantics: ghost = value at the wrapped coordinates).  The image path is
-// rare (points within h of a wrapped face).
-template <int NOUT>
-__device__ __forceinline__ void emit(double* out, const Geom& g, int i, int j, int k,
-                                     const double* val, int wrap_mask) {
-  const int h = g.h;
-  double* o = out + ((int64_t)(i + h) * g.s0 + (int64_t)(j + h) * g.s1 + (k + h));
+    for (int f = 0; f < NOUT; ++f) out[f * g.fs + c] = val[f];
+  }
+  if (ni * nj * nk > 1) {
+    for (int a = 0; a < ni; ++a)
+      for (int b = 0; b < nj; ++b)
+        for (int d = 0; d < nk; ++d) {
+          if ((a | b | d) == 0) continue;
+          const int64_t c = ci[a] * g.s0 + cj[b] * g.s1 + ck[d];
 #pragma unroll
-  for (int f = 0; f < NOUT; ++f) o[f * g.fs] = val[f];
-  const bool img = ((wrap_mask & 1) && (i < h || i >= g.n0 - h)) ||
-                   ((wrap_mask & 2) && (j < h || j >= g.n1 - h)) ||
-                   ((wrap_mask & 4) && (k < h || k >= g.n2 - h));
-  if (img) emit_ghosts<NOUT>(out, g, i, j, k, val, wrap_mask);
+          for (int f = 0; f < NOUT; ++f) out[f * g.fs + c] = val[f];
+        }
+  }
 }
 
 // Arrival conversion of one staged plane slot (all PLANE points of the box):
