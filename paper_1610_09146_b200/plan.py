@@ -97,6 +97,75 @@ def plan_storage(plan: KernelPlan, spec=None) -> dict:
     return out
 
 
+def stencil_applications_per_point(plan: KernelPlan) -> int:
+    """Stencil applications per grid point per residual evaluation, counted
+    as the reference does (plan.py:248-264): FETCH costs 1 (the fill), LOCAL
+    costs 1 (5 for a mixed term whose inner derivative is not stored),
+    INLINE costs that times the derivative's occurrences in the residuals."""
+    storage = plan_storage(plan)
+    total = 0
+    for did, cls in storage.items():
+        cross = did.startswith("DD(")
+        inner_stored = False
+        if cross:
+            j = did[4]
+            inner_stored = storage[f"D(u{j},x{j})"] == FETCH
+        cost = 5 if cross and not inner_stored else 1
+        if cls == FETCH:
+            total += 1
+        elif cls == LOCAL:
+            total += cost
+        else:
+            total += OCCURRENCES[did] * cost
+    return total
+
+
+# Occurrences of each derivative in the five residual expressions
+# (terms.py:190-193), as the reference's term list spells them.
+def _occurrences() -> dict:
+    occ = {d: 0 for d in derivative_ids()}
+    for j in range(3):          # mass
+        occ[f"D(rhou{j},x{j})"] += 1
+        occ[f"D(rho,x{j})"] += 1
+        occ[f"D(u{j},x{j})"] += 1
+    for i in range(3):          # momentum i
+        for j in range(3):
+            occ[f"D(rhou{i}*u{j},x{j})"] += 1
+            occ[f"D(rhou{i},x{j})"] += 1
+            occ[f"D(u{j},x{j})"] += 1
+        occ[f"D(p,x{i})"] += 1
+        occ[f"D2(u{i},x{i})"] += 1
+        for j in range(3):
+            if j != i:
+                occ[f"D2(u{i},x{j})"] += 1
+                occ[f"DD(u{j},x{i},x{j})"] += 1
+    for j in range(3):          # energy: convection, pressure work, heat
+        occ[f"D(rhoe*u{j},x{j})"] += 1
+        occ[f"D(rhoe,x{j})"] += 1
+        occ[f"D(u{j},x{j})"] += 1
+        occ[f"D(u{j}*p,x{j})"] += 1
+        occ[f"D2(T,x{j})"] += 1
+    for i in range(3):          # stress work: tau_ij * D(u_i, x_j)
+        for j in range(3):
+            if i == j:
+                occ[f"D(u{i},x{i})"] += 2
+                for q in range(3):
+                    occ[f"D(u{q},x{q})"] += 1
+            else:
+                occ[f"D(u{i},x{j})"] += 2
+                occ[f"D(u{j},x{i})"] += 1
+    for i in range(3):          # u_i * viscous_i
+        occ[f"D2(u{i},x{i})"] += 1
+        for j in range(3):
+            if j != i:
+                occ[f"D2(u{i},x{j})"] += 1
+                occ[f"DD(u{j},x{i},x{j})"] += 1
+    return occ
+
+
+OCCURRENCES = _occurrences()
+
+
 def workarray_budget(plan: KernelPlan, spec=None) -> int:
     """Grid-sized derivative arrays the plan allocates in HBM.
 

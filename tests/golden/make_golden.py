@@ -140,6 +140,16 @@ def main():
         "u0": float(ka.u[0].interior[0, 0, 0]),
         "p": float(ka.p.interior[0, 0, 0]),
         "T": float(ka.T.interior[0, 0, 0])}
+    # plan introspection (terms.py:190-193, plan.py:220-264)
+    from fdns import terms
+    from fdns.plan import build_plan, lower_plan, workarray_budget
+    spec = terms.build_residual_spec()
+    meta["occurrences"] = dict(spec.occurrences)
+    meta["stencil_applications_per_point"] = {
+        n: lower_plan(build_plan(n)).stencil_applications_per_point()
+        for n in PLAN_NAMES}
+    meta["workarray_budget"] = {n: workarray_budget(build_plan(n))
+                                for n in PLAN_NAMES}
     meta["constants"] = {"gm1": C.gm1, "gM2": C.gM2, "inv_Re": C.inv_Re,
                          "heat_coeff": C.heat_coeff, "c13": C.c13_inv_Re,
                          "c43": C.c43_inv_Re, "c23": C.c23_inv_Re}

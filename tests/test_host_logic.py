@@ -152,3 +152,20 @@ def test_no_cpu_fallback_without_gpu(built):
     g = fd.make_grid((8, 8, 8), (2 * math.pi,) * 3)
     with pytest.raises(_lib.FdnsError):
         fd.taylor_green_init(g, fd.PhysicalConstants())
+
+
+def test_plan_introspection_matches_reference(built, golden_meta):
+    """Occurrence counts, stencil applications per point and work-array
+    budgets against the values the reference itself reports
+    (terms.py:190-193, plan.py:220-264; tests/golden/make_golden.py)."""
+    from paper_1610_09146_b200.plan import (OCCURRENCES,
+                                            stencil_applications_per_point)
+    assert OCCURRENCES == golden_meta["occurrences"]
+    for name, want in golden_meta["stencil_applications_per_point"].items():
+        assert stencil_applications_per_point(fd.build_plan(name)) == want
+    ref = golden_meta["workarray_budget"]
+    assert ref == {"BL": 61, "RA": 0, "RS": 9, "SN": 0, "SS": 9}
+    # identical except BL's product scratch array, which this design drops
+    for name in fd.PLAN_NAMES:
+        assert fd.workarray_budget(fd.build_plan(name)) == \
+            ref[name] - (1 if name == "BL" else 0)
