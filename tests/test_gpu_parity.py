@@ -382,3 +382,50 @@ def test_slab_decomposition_bitwise_invariant(variant, nranks, split):
                 exchange(dst[k])
     got = np.concatenate([host_cons(st) for st in states], axis=1)
     assert np.array_equal(got, want)
+
+
+# ------------------------------------------- bounds (compute-sanitizer is closed)
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("npts", [(12, 16, 20), (9, 12, 7)])
+def test_no_writes_outside_bundles(variant, npts):
+    """Run the fused stage and the residual through the raw C ABI on
+    bundles embedded in larger buffers pre-filled with a NaN-payload canary:
+    every byte outside the output bundle, and the residual's halo (the
+    reference leaves it zero, plan.py:413-415), must be untouched."""
+    from paper_1610_09146_b200 import _lib
+    lib = _lib.load()
+    F = npo.manufactured(npts, CO)
+    g = grid_of(npts)
+    pb = g.problem(C)
+    fs = int(np.prod(g.shape))
+    pad = 4096
+    canary = np.frombuffer(np.uint64(0x7FF8DEADBEEF0001).tobytes(), dtype=np.float64)[0]
+
+    def framed(nf):
+        buf = torch.full((nf * fs + 2 * pad,), canary, dtype=torch.float64, device="cuda")
+        return buf, buf[pad:pad + nf * fs].view((nf,) + g.shape)
+
+    nw = lib.fdns_workarray_count(_lib.VARIANT_IDS[variant])
+    src_buf, src = framed(10)
+    src.copy_(torch.from_numpy(F))
+    out_buf, out = framed(10)
+    out.zero_()
+    work_buf, work = framed(max(nw, 1))
+    res_buf, res = framed(5)
+    res.zero_()
+    _lib.check(lib.fdns_stage(_lib.VARIANT_IDS[variant], _lib.ptr(src), _lib.ptr(src),
+                              _lib.ptr(out), _lib.ptr(work), 1e-3, 7, pb,
+                              _lib.stream_handle()))
+    _lib.check(lib.fdns_residual(_lib.VARIANT_IDS[variant], _lib.ptr(src), _lib.ptr(work),
+                                 _lib.ptr(res), pb, _lib.stream_handle()))
+    torch.cuda.synchronize()
+    for buf in (src_buf, out_buf, work_buf, res_buf):
+        h = buf.cpu().numpy().view(np.uint64)
+        assert (h[:pad] == 0x7FF8DEADBEEF0001).all()
+        assert (h[-pad:] == 0x7FF8DEADBEEF0001).all()
+    assert np.array_equal(src.cpu().numpy(), F)          # input untouched
+    r = res.cpu().numpy()
+    assert np.all(r[:, :2] == 0) and np.all(r[:, -2:] == 0)
+    assert np.all(r[:, :, :2] == 0) and np.all(r[:, :, :, -2:] == 0)
+    want = c_oracle.residual(F, CO)
+    assert np.array_equal(npo.interior(r, 2), want)
