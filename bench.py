@@ -67,8 +67,9 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap,power.draw")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 100):
         self.index = index
+        self.period_ms = period_ms
         self.rows = []
         self.proc = None
 
@@ -76,7 +77,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -148,7 +149,8 @@ def run_cpu_oracle(n: int, steps: int, warmup: int = 1, min_seconds: float = 0.0
 
 
 # ------------------------------------------------------------------ ours
-def bench_variant(fd, variant, grid, steps, warmup, flush_buf, lib):
+def bench_variant(fd, variant, grid, steps, warmup, flush_buf, lib, clocks=None,
+                  clock_window=0.0):
     import torch
     from paper_1610_09146_b200 import _lib
     from paper_1610_09146_b200.timeloop import IterationState, _fused_iteration
@@ -182,6 +184,16 @@ def bench_variant(fd, variant, grid, steps, warmup, flush_buf, lib):
             _fused_iteration(it, scheme, ev)
 
     stream = torch.cuda.current_stream()
+    if clock_window > 0:
+        # untimed replay of the same step, long enough for nvidia-smi to
+        # sample the clocks under exactly this load (the timed K steps below
+        # last only milliseconds)
+        with clocks:
+            t_end = time.perf_counter() + clock_window
+            while time.perf_counter() < t_end:
+                for _ in range(20):
+                    step()
+                torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True),
             torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     n_launch0 = lib.fdns_launch_count()
@@ -360,10 +372,12 @@ def main_ours(args):
 
     fp64_tf = fp64_peak(lib)
     results = {}
-    with ClockSampler(local) as clocks:
+    clocks = ClockSampler(local, period_ms=20)
+    if True:
         for v in args.variants:
             total_ms, launches, stage_ms = bench_variant(
-                fd, v, grid, args.steps, args.warmup, flush, lib)
+                fd, v, grid, args.steps, args.warmup, flush, lib, clocks,
+                args.clock_window)
             if world > 1:
                 import torch.distributed as dist
                 t = torch.tensor([total_ms, stage_ms], device="cuda")
@@ -439,7 +453,9 @@ def main_ours(args):
         "stage_sweep": sizes,
         "e2e": e2e,
         "gpu_launches": r["gpu_launches"],
-        "clocks": clocks.summary(),
+        "clocks": {**clocks.summary(),
+                   "window": f"{args.clock_window:.1f} s replay of each "
+                             "variant's step right before its timed region"},
     }
     print(json.dumps(line))
 
@@ -483,6 +499,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="minimum timed CPU work for the baseline sample")
+    ap.add_argument("--clock-window", type=float, default=0.5,
+                    help="seconds of untimed step replay sampled for clocks")
     ap.add_argument("--sizes", default="128,256",
                     help="extra grid sizes for the steady-state stage sweep")
     ap.add_argument("--no-cpu", action="store_true")
