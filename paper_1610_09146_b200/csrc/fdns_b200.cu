@@ -229,34 +229,47 @@ __global__ void __launch_bounds__(256) k_fill_bl_all(const double* __restrict__ 
 // come from the fill kernels).  Together they hold exactly what the
 // reference's halo-exchanged inner arrays hold (plan.py:378-379).
 template <int Q>
-__global__ void k_diag_ghost(const double* __restrict__ in, double* __restrict__ dst, Coef k,
-                             Geom g) {
+__device__ __forceinline__ void diag_ghost_point(const double* __restrict__ in,
+                                                 double* __restrict__ dst, const Coef& k,
+                                                 const Geom& g, int64_t t) {
   const int h = g.h;
   const int n[3] = {g.n0, g.n1, g.n2};
   constexpr int A = Q == 0 ? 1 : 0;   // the two other axes, A < B
   constexpr int B = Q == 2 ? 1 : 2;
-  const int PA = n[A] + 2 * h, PB = n[B] + 2 * h;
+  const int PB = n[B] + 2 * h;
   const int64_t frame = (int64_t)2 * h * PB + (int64_t)n[A] * 2 * h;
-  const int64_t total = frame * n[Q];
+  const int q = (int)(t / frame) + h;
+  int64_t f = t % frame;
+  int ca, cb;
+  if (f < (int64_t)2 * h * PB) {            // ghost rows of axis A, all of B
+    ca = (int)(f / PB); cb = (int)(f % PB);
+    ca = ca < h ? ca : n[A] + ca;
+  } else {                                   // interior A, ghost columns of B
+    f -= (int64_t)2 * h * PB;
+    ca = (int)(f / (2 * h)) + h; cb = (int)(f % (2 * h));
+    cb = cb < h ? cb : n[B] + cb;
+  }
+  int idx[3];
+  idx[Q] = q; idx[A] = ca; idx[B] = cb;
+  const int64_t c = idx[0] * g.s0 + idx[1] * g.s1 + idx[2];
+  GAcc a{in, c, g.s0, g.s1, g.fs};
+  dst[c] = d1<Q, E_FIELD, U0 + Q, 0>(k, a);
+}
+
+// D(u_q, x_q) on the ghost frames of all three diagonal arrays in one
+// launch: points whose axis-q coordinate is interior while another
+// coordinate lies in the halo (the interior values come from the fill
+// kernels).  Together they hold exactly what the reference's halo-exchanged
+// inner arrays hold (plan.py:378-379).
+__global__ void k_diag_ghost(const double* __restrict__ in, double* __restrict__ d0,
+                             double* __restrict__ d1p, double* __restrict__ d2p, Coef k, Geom g,
+                             int64_t f0, int64_t f1, int64_t f2) {
+  const int64_t total = f0 + f1 + f2;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int q = (int)(t / frame) + h;
-    int64_t f = t % frame;
-    int ca, cb;
-    if (f < (int64_t)2 * h * PB) {            // ghost rows of axis A, all of B
-      ca = (int)(f / PB); cb = (int)(f % PB);
-      ca = ca < h ? ca : n[A] + ca;
-    } else {                                   // interior A, ghost columns of B
-      f -= (int64_t)2 * h * PB;
-      ca = (int)(f / (2 * h)) + h; cb = (int)(f % (2 * h));
-      cb = cb < h ? cb : n[B] + cb;
-    }
-    (void)PA;
-    int idx[3];
-    idx[Q] = q; idx[A] = ca; idx[B] = cb;
-    const int64_t c = idx[0] * g.s0 + idx[1] * g.s1 + idx[2];
-    GAcc a{in, c, g.s0, g.s1, g.fs};
-    dst[c] = d1<Q, E_FIELD, U0 + Q, 0>(k, a);
+    if (t < f0) diag_ghost_point<0>(in, d0, k, g, t);
+    else if (t < f0 + f1) diag_ghost_point<1>(in, d1p, k, g, t - f0);
+    else diag_ghost_point<2>(in, d2p, k, g, t - f0 - f1);
   }
 }
 
@@ -544,10 +557,8 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
     const int64_t f0 = (int64_t)g.n0 * (2 * h * (g.n2 + 2 * h) + (int64_t)g.n1 * 2 * h);
     const int64_t f1 = (int64_t)g.n1 * (2 * h * (g.n2 + 2 * h) + (int64_t)g.n0 * 2 * h);
     const int64_t f2 = (int64_t)g.n2 * (2 * h * (g.n1 + 2 * h) + (int64_t)g.n0 * 2 * h);
-    auto nb = [](int64_t t) { return (int)std::min<int64_t>((t + 255) / 256, 148 * 8); };
-    k_diag_ghost<0><<<nb(f0), 256, 0, s>>>(in, d0, k, g);
-    k_diag_ghost<1><<<nb(f1), 256, 0, s>>>(in, d1p, k, g);
-    k_diag_ghost<2><<<nb(f2), 256, 0, s>>>(in, d2p, k, g);
+    const int nb = (int)std::min<int64_t>((f0 + f1 + f2 + 255) / 256, 148 * 8);
+    k_diag_ghost<<<nb, 256, 0, s>>>(in, d0, d1p, d2p, k, g, f0, f1, f2);
   };
   if (variant == FDNS_BL) {
     // (a TMA-staged fill, k_stage_tiled<BL, 2>, measured 1.6x slower at
@@ -556,13 +567,13 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
     ghosts(work + slot(0, S_U + 0) * g.fs, work + slot(1, S_U + 1) * g.fs,
            work + slot(2, S_U + 2) * g.fs);
     k_fill_cross<<<grd, blk, 0, s>>>(work, k, g);
-    count(5);
+    count(3);
     return check_launch("BL fills");
   }
   if (variant == FDNS_SS || variant == FDNS_RS) {
     k_grad_ss<<<grd, blk, 0, s>>>(in, work, k, g);
     ghosts(work + 0 * g.fs, work + 4 * g.fs, work + 8 * g.fs);
-    count(4);
+    count(2);
     return check_launch("SS fills");
   }
   return 0;
