@@ -292,25 +292,39 @@ __global__ void __launch_bounds__(256, 4) k_fill_cross(double* __restrict__ wa, 
   }
 }
 
-// SS/RS fill: the six off-diagonal velocity gradients on the interior
-// (diagonals come from k_diag_ext).  ws[q*3+a] = D(u_q, x_a).
-__global__ void __launch_bounds__(256, 4) k_grad_ss(const double* __restrict__ in,
-                                                 double* __restrict__ ws, Coef k, Geom g) {
-  const int kk = blockIdx.x * blockDim.x + threadIdx.x;
-  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
-  const int ii = blockIdx.z;
-  if (kk >= g.n2 || jj >= g.n1) return;
-  const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
-  GAcc a{in, c, g.s0, g.s1, g.fs};
-  ws[(0 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U0, 0>(k, a);
-  ws[(1 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U1, 0>(k, a);
-  ws[(2 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U2, 0>(k, a);
-  ws[(0 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U0, 0>(k, a);
-  ws[(0 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U0, 0>(k, a);
-  ws[(1 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U1, 0>(k, a);
-  ws[(1 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U1, 0>(k, a);
-  ws[(2 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U2, 0>(k, a);
-  ws[(2 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U2, 0>(k, a);
+// SS/RS fill in one launch: the nine velocity gradients ws[q*3+a] =
+// D(u_q, x_a) on the interior, then the ghost frames of the three diagonal
+// ones (k_diag_ghost semantics).
+__global__ void __launch_bounds__(256) k_grad_ss_all(const double* __restrict__ in,
+                                                     double* __restrict__ ws, Coef k, Geom g,
+                                                     int64_t nint, int64_t f0, int64_t f1,
+                                                     int64_t f2) {
+  const int64_t total = nint + f0 + f1 + f2;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < nint) {
+      const int kk = (int)(t % g.n2);
+      const int64_t u = t / g.n2;
+      const int jj = (int)(u % g.n1);
+      const int ii = (int)(u / g.n1);
+      const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
+      GAcc a{in, c, g.s0, g.s1, g.fs};
+      ws[(0 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U0, 0>(k, a);
+      ws[(0 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U0, 0>(k, a);
+      ws[(0 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U0, 0>(k, a);
+      ws[(1 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U1, 0>(k, a);
+      ws[(1 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U1, 0>(k, a);
+      ws[(1 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U1, 0>(k, a);
+      ws[(2 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U2, 0>(k, a);
+      ws[(2 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U2, 0>(k, a);
+      ws[(2 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U2, 0>(k, a);
+    } else {
+      const int64_t x = t - nint;
+      if (x < f0) diag_ghost_point<0>(in, ws + 0 * g.fs, k, g, x);
+      else if (x < f0 + f1) diag_ghost_point<1>(in, ws + 4 * g.fs, k, g, x - f0);
+      else diag_ghost_point<2>(in, ws + 8 * g.fs, k, g, x - f0 - f1);
+    }
+  }
 }
 
 // RK update on the interior of 5 fields (timeloop.py:80-85).
@@ -571,9 +585,16 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
     return check_launch("BL fills");
   }
   if (variant == FDNS_SS || variant == FDNS_RS) {
-    k_grad_ss<<<grd, blk, 0, s>>>(in, work, k, g);
-    ghosts(work + 0 * g.fs, work + 4 * g.fs, work + 8 * g.fs);
-    count(2);
+    {   // 9 gradients on the interior + the diagonal ghost frames, one launch
+      const int h = g.h;
+      const int64_t nint = (int64_t)g.n0 * g.n1 * g.n2;
+      const int64_t f0 = (int64_t)g.n0 * (2 * h * (g.n2 + 2 * h) + (int64_t)g.n1 * 2 * h);
+      const int64_t f1 = (int64_t)g.n1 * (2 * h * (g.n2 + 2 * h) + (int64_t)g.n0 * 2 * h);
+      const int64_t f2 = (int64_t)g.n2 * (2 * h * (g.n1 + 2 * h) + (int64_t)g.n0 * 2 * h);
+      const int nb = (int)std::min<int64_t>((nint + f0 + f1 + f2 + 255) / 256, 148 * 16);
+      k_grad_ss_all<<<nb, 256, 0, s>>>(in, work, k, g, nint, f0, f1, f2);
+    }
+    count(1);
     return check_launch("SS fills");
   }
   return 0;
