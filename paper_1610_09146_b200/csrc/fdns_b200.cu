@@ -152,9 +152,6 @@ __global__ void k_halo_wrap(double* __restrict__ F, int nf, int mask, Geom g, in
 // Point-kernel residual (one thread per interior point), all variants.
 // Mode: 0 = write residual, 1 = fused RK update + primitives.
 // ---------------------------------------------------------------------------
-template <int V>
-struct VariantTag {};
-
 template <int V, int MODE>
 __global__ void __launch_bounds__(256) k_residual(const double* __restrict__ in,
                                                   const double* saved, double* out,

@@ -11,9 +11,12 @@
 // The derivative *provider* decides where a derivative value comes from,
 // which is exactly what distinguishes the paper's variants:
 //   LocalProvider   (SN)  every distinct derivative evaluated once, kept live
+//                         (point kernels; the tiled kernels use the lazily
+//                         evaluated TiledLazyProvider, fdns_tiled.cuh)
 //   InlineProvider  (RA)  re-expanded from the stencil at every occurrence
 //   FetchProvider   (BL)  read from a stored work array
 //   SSProvider      (SS)  9 velocity gradients stored, the rest local
+//                   (RS)  the same with the rest re-expanded (INLINE)
 // The residual body (residual_point) is written once over the provider API.
 #pragma once
 #include <cstdint>
