@@ -429,3 +429,65 @@ def test_no_writes_outside_bundles(variant, npts):
     assert np.all(r[:, :, :2] == 0) and np.all(r[:, :, :, -2:] == 0)
     want = c_oracle.residual(F, CO)
     assert np.array_equal(npo.interior(r, 2), want)
+
+
+# --------------------------------------------------- C4 / C5 / edge cases
+@pytest.mark.parametrize("variant", ["RA", "SS"])
+def test_c4_256_steps_match_c_oracle(variant):
+    """Config C4's grid and variants (TGV 256^3, dt=8.5e-4, RA and SS): five
+    RK3 steps on the GPU bitwise equal to the C oracle (the 100-step and
+    multi-GPU parts are covered by C2/C3 hashes and the decomposition
+    invariance tests)."""
+    n, steps, dt = 256, 5, 8.5e-4
+    F = npo.taylor_green(n, CO)
+    G = F.copy()
+    c_oracle.run(G, CO, dt, steps)
+    g = grid_of((n,) * 3)
+    st = state_from_cons(g, npo.interior(F[:5], 2))
+    fd.run(st, fd.RKScheme(dt=dt), fd.ResidualEvaluator(g, C, variant), steps)
+    assert np.array_equal(host_cons(st), npo.interior(G[:5], 2))
+
+
+def test_c5_512_cross_variant_bitwise():
+    """Config C5 on one GPU (TGV 512^3, dt=4.2e-4, all four variants; BL's
+    60 work arrays put it at ~99 GB of HBM): one RK3 step, all variants
+    bitwise equal (512^3+ parity rests on cross-variant and
+    decomposition invariance)."""
+    n, dt = 512, 4.2e-4
+    g = grid_of((n,) * 3)
+    ref = None
+    for v in NS_VARIANTS:
+        st = fd.taylor_green_init(g, C)
+        ev = fd.ResidualEvaluator(g, C, v)
+        fd.run(st, fd.RKScheme(dt=dt), ev, 1)
+        got = st.bundle[:5].clone()
+        del st, ev
+        torch.cuda.empty_cache()
+        if ref is None:
+            ref = got
+        else:
+            assert torch.equal(got, ref), v
+    assert torch.isfinite(ref).all()
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_halo_width_three_and_box_lengths(variant):
+    """Halo width 3 (mesh.py:82 allows any h >= 2) and a non-cubic, non-2*pi
+    box: residual and one fused step bitwise equal to the oracle."""
+    npts, h = (12, 10, 14), 3
+    lengths = (1.0, 2.5, 0.75)
+    g = fd.make_grid(npts, lengths, halo=h)
+    rng = np.random.default_rng(4)
+    shape = npts
+    rho = 1.0 + 0.1 * rng.random(shape)
+    u = [0.2 * rng.standard_normal(shape) for _ in range(3)]
+    p = 70.0 + rng.random(shape)
+    F = npo.state_from_primitives(npts, CO, rho, u, p, h=h)
+    st = fd.ConservativeState(g)
+    st.bundle[:5].copy_(torch.from_numpy(F[:5]))
+    fd.eval_primitives_fused(st, C)
+    assert np.array_equal(st.to_numpy(), F)
+    w = [npo.weights(l / n) for l, n in zip(lengths, npts)]
+    want = np.stack(npo.residual(F, h, w, CO))
+    got = fd.assemble_residual(st, C, variant).interior_numpy()
+    assert np.array_equal(got, want)
