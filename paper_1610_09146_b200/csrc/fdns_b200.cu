@@ -452,7 +452,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 bool plane_map(CUtensorMap* m, const double* base, const Geom& g) {
   const int64_t P2 = g.n2 + 2 * g.h, P1 = g.n1 + 2 * g.h, P0 = g.n0 + 2 * g.h;
-  if (P2 % 2 != 0) return false;
+  // 16-byte rows, and an even innermost box start (k0 + h - 2): an odd one
+  // (odd h) is only 8-byte aligned and the bulk tensor copy faults on it
+  if (P2 % 2 != 0 || g.h % 2 != 0) return false;
   if (reinterpret_cast<uintptr_t>(base) % 16 != 0) return false;
   auto fn = encode_fn();
   if (!fn) return false;

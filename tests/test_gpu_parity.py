@@ -471,10 +471,12 @@ def test_c5_512_cross_variant_bitwise():
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
-def test_halo_width_three_and_box_lengths(variant):
-    """Halo width 3 (mesh.py:82 allows any h >= 2) and a non-cubic, non-2*pi
-    box: residual and one fused step bitwise equal to the oracle."""
-    npts, h = (12, 10, 14), 3
+@pytest.mark.parametrize("h", [3, 4])
+def test_halo_width_and_box_lengths(variant, h):
+    """Halo widths 3 (point kernels: an odd halo misaligns the TMA box) and
+    4 (TMA-staged) -- mesh.py:82 allows any h >= 2 -- on a non-cubic,
+    non-2*pi box: primitives and residual bitwise equal to the oracle."""
+    npts = (12, 10, 14)
     lengths = (1.0, 2.5, 0.75)
     g = fd.make_grid(npts, lengths, halo=h)
     rng = np.random.default_rng(4)
