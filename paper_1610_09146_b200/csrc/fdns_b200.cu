@@ -480,6 +480,27 @@ int num_sms() {
   return g_num_sms;
 }
 
+// Persistent grid size: one CTA per SM, at least ~4 plane steps each.  When
+// the grid has at least as many CTAs as tiles the split is tile-aligned
+// (Segments::partition); pick the CTA count in [tiles, SMs] that minimises
+// the longest CTA (max plane steps + one ramp).
+int64_t pick_ctas(int64_t tiles, int planes) {
+  const int64_t total = tiles * planes;
+  if (g_tiled_ctas > 0) return std::min<int64_t>(g_tiled_ctas, total);
+  const int64_t sms = num_sms();
+  int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(sms, total / 4));
+  if (ctas < tiles) return ctas;
+  int64_t best = ctas, best_len = INT64_MAX;
+  for (int64_t G = tiles; G <= ctas; ++G) {
+    const int64_t m = (G + tiles - 1) / tiles;            // most CTAs on a tile
+    const int64_t mmin = G / tiles;                       // fewest
+    const int64_t len = (planes + mmin - 1) / mmin;       // longest range
+    (void)m;
+    if (len < best_len || (len == best_len && G < best)) { best_len = len; best = G; }
+  }
+  return best;
+}
+
 template <int V, int MODE, bool LAZY = true>
 int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const double* work,
                    const Coef& k, const Geom& g, double coef, int wrap, int i_lo, int i_hi,
@@ -495,9 +516,7 @@ int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const
   const int ntj = (g.n1 + tiled::TJ - 1) / tiled::TJ;
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
-  // one persistent CTA per SM, each at least ~4 plane steps
-  int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(num_sms(), total / 4));
-  if (g_tiled_ctas > 0) ctas = std::min<int64_t>(g_tiled_ctas, total);
+  const int64_t ctas = pick_ctas(ntk * ntj, nplanes);
   tiled::k_stage_tiled<V, MODE, LAZY><<<(unsigned)ctas, tiled::NT, smem, s>>>(
       m, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes);
   return 0;
@@ -516,8 +535,7 @@ int launch_sn2(const CUtensorMap& m, const double* saved, double* out, const Coe
   const int ntj = (g.n1 + tiled::TJ - 1) / tiled::TJ;
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
-  int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(num_sms(), total / 4));
-  if (g_tiled_ctas > 0) ctas = std::min<int64_t>(g_tiled_ctas, total);
+  const int64_t ctas = pick_ctas(ntk * ntj, nplanes);
   sn2::k_stage_sn2<MODE><<<(unsigned)ctas, sn2::NT, sn2::SMEM_BYTES, s>>>(
       m, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes);
   return 0;

@@ -92,8 +92,7 @@ __global__ void __launch_bounds__(NT, 1)
   const bool groupB = tid >= NPT;
   const int pt = groupB ? tid - NPT : tid;
   const int tk = pt % TK, tj = pt / TK;
-  tiled::Segments S{blockIdx.x * total_steps / gridDim.x,
-                    (blockIdx.x + 1) * total_steps / gridDim.x, nplanes};
+  tiled::Segments S = tiled::Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes);
   if (S.beg >= S.end) return;
 
   if (tid == 0) {

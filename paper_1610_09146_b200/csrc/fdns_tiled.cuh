@@ -272,6 +272,28 @@ struct Segments {
     const int64_t tile_end = (x / n0 + 1) * (int64_t)n0;
     return tile_end < end ? tile_end : end;
   }
+  // CTA b of G over `total` = tiles * planes steps.  With at least as many
+  // CTAs as tiles, split tile-aligned (each tile gets floor or ceil of
+  // G/tiles CTAs, each CTA one contiguous plane range of one tile: one
+  // pipeline ramp per CTA); otherwise equal contiguous ranges in tile-major
+  // order (a CTA may span tiles; its ramps amortise over many planes).
+  static __device__ __forceinline__ Segments partition(int64_t b, int64_t G, int64_t total,
+                                                       int planes) {
+    const int64_t tiles = total / planes;
+    if (G >= tiles) {
+      const int64_t base = G / tiles, rem = G % tiles;
+      int64_t t, r, m;
+      if (b < rem * (base + 1)) {
+        t = b / (base + 1); r = b % (base + 1); m = base + 1;
+      } else {
+        const int64_t b2 = b - rem * (base + 1);
+        t = rem + b2 / base; r = b2 % base; m = base;
+      }
+      const int64_t p0 = r * planes / m, p1 = (r + 1) * planes / m;
+      return Segments{t * planes + p0, t * planes + p1, planes};
+    }
+    return Segments{b * total / G, (b + 1) * total / G, planes};
+  }
 };
 
 template <int V, int MODE, bool LAZY = true>
@@ -285,8 +307,7 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NR * SLOT + (kBuf ? 2 * NBUF * PLANE : 0));
   const int tid = threadIdx.x;
   const int tk = tid % TK, tj = tid / TK;
-  Segments S{blockIdx.x * total_steps / gridDim.x, (blockIdx.x + 1) * total_steps / gridDim.x,
-             nplanes};
+  Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes);
   if (S.beg >= S.end) return;
 
   if (tid == 0) {
