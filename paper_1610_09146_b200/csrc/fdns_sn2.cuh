@@ -84,7 +84,7 @@ template <int MODE>
 __global__ void __launch_bounds__(NT, 1)
     k_stage_sn2(const __grid_constant__ CUtensorMap tin, const double* saved, double* out,
                 Coef k, Geom g, double coef, int ntk, int64_t total_steps, int wrap_mask,
-                int i_lo, int nplanes) {
+                int i_lo, int nplanes, int aligned) {
   extern __shared__ __align__(128) double sm[];
   double* bset0 = sm + NR * SLOT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(bset0 + 2 * BSET);
@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(NT, 1)
   const bool groupB = tid >= NPT;
   const int pt = groupB ? tid - NPT : tid;
   const int tk = pt % TK, tj = pt / TK;
-  tiled::Segments S = tiled::Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes);
+  tiled::Segments S = tiled::Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes,
+                                                   aligned);
   if (S.beg >= S.end) return;
 
   if (tid == 0) {

@@ -272,15 +272,15 @@ struct Segments {
     const int64_t tile_end = (x / n0 + 1) * (int64_t)n0;
     return tile_end < end ? tile_end : end;
   }
-  // CTA b of G over `total` = tiles * planes steps.  With at least as many
-  // CTAs as tiles, split tile-aligned (each tile gets floor or ceil of
+  // CTA b of G over `total` = tiles * planes steps.  `aligned` (needs at
+  // least as many CTAs as tiles): split tile-aligned (each tile gets floor or ceil of
   // G/tiles CTAs, each CTA one contiguous plane range of one tile: one
   // pipeline ramp per CTA); otherwise equal contiguous ranges in tile-major
   // order (a CTA may span tiles; its ramps amortise over many planes).
   static __device__ __forceinline__ Segments partition(int64_t b, int64_t G, int64_t total,
-                                                       int planes) {
+                                                       int planes, int aligned) {
     const int64_t tiles = total / planes;
-    if (G >= tiles) {
+    if (aligned && G >= tiles) {
       const int64_t base = G / tiles, rem = G % tiles;
       int64_t t, r, m;
       if (b < rem * (base + 1)) {
@@ -300,14 +300,15 @@ template <int V, int MODE, bool LAZY = true>
 __global__ void __launch_bounds__(NT, 1)
     k_stage_tiled(const __grid_constant__ CUtensorMap tin, const double* __restrict__ work,
                   const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
-                  int64_t total_steps, int wrap_mask, int i_lo, int nplanes) {
+                  int64_t total_steps, int wrap_mask, int i_lo, int nplanes, int aligned) {
   extern __shared__ __align__(128) double sm[];
   constexpr bool kBuf = (V == FDNS_SN);
   double* bufs0 = sm + NR * SLOT;   // 2 x NBUF planes (SN only)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NR * SLOT + (kBuf ? 2 * NBUF * PLANE : 0));
   const int tid = threadIdx.x;
   const int tk = tid % TK, tj = tid / TK;
-  Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes);
+  Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes,
+                                                   aligned);
   if (S.beg >= S.end) return;
 
   if (tid == 0) {
