@@ -450,6 +450,25 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// The three diagonal velocity gradients of an SS/RS work bundle (fields 0,
+// 4, 8: D(u_q, x_q)) as a 4-D tensor with a field stride of 4 fields.
+bool grad_map(CUtensorMap* m, const double* work, const Geom& g) {
+  const int64_t P2 = g.n2 + 2 * g.h, P1 = g.n1 + 2 * g.h, P0 = g.n0 + 2 * g.h;
+  if (P2 % 2 != 0 || g.h % 2 != 0) return false;
+  if (reinterpret_cast<uintptr_t>(work) % 16 != 0) return false;
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)P2, (cuuint64_t)P1, (cuuint64_t)P0, 3};
+  cuuint64_t strides[3] = {(cuuint64_t)(P2 * 8), (cuuint64_t)(P1 * P2 * 8),
+                           (cuuint64_t)(4 * g.fs * 8)};
+  cuuint32_t box[4] = {tiled::PK, tiled::PJ, 1, tiled::NGB};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(work), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool plane_map(CUtensorMap* m, const double* base, const Geom& g) {
   const int64_t P2 = g.n2 + 2 * g.h, P1 = g.n1 + 2 * g.h, P0 = g.n0 + 2 * g.h;
   // 16-byte rows, and an even innermost box start (k0 + h - 2): an odd one
@@ -508,7 +527,12 @@ template <int V, int MODE, bool LAZY = true>
 int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const double* work,
                    const Coef& k, const Geom& g, double coef, int wrap, int i_lo, int i_hi,
                    cudaStream_t s) {
-  constexpr int smem = V == FDNS_SN ? tiled::SMEM_BYTES_SN : tiled::SMEM_BYTES;
+  constexpr bool gb = (V == FDNS_SS || V == FDNS_RS) && MODE != 2;
+  constexpr int smem = V == FDNS_SN ? tiled::SMEM_BYTES_SN
+                                    : (gb ? tiled::SMEM_BYTES_SS : tiled::SMEM_BYTES);
+  CUtensorMap mg = m;
+  if constexpr (gb)
+    if (!grad_map(&mg, work, g)) return fail("gradient tensor map");
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tiled::k_stage_tiled<V, MODE, LAZY>,
@@ -521,7 +545,7 @@ int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const
   const int64_t total = (int64_t)ntk * ntj * nplanes;
   const Launch L = pick_launch(ntk * ntj, nplanes);
   tiled::k_stage_tiled<V, MODE, LAZY><<<(unsigned)L.ctas, tiled::NT, smem, s>>>(
-      m, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes, L.aligned);
+      m, mg, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes, L.aligned);
   return 0;
 }
 

@@ -177,6 +177,12 @@ constexpr int BU2_N = PJ * TK;          // D(u2,x2): all rows, interior columns
 constexpr int BUF_WORK = PLANE + BU1_N + BU2_N;
 constexpr int SMEM_BYTES_SN = NR * SLOT * 8 + 2 * NBUF * PLANE * 8 + 128;
 static_assert(SMEM_BYTES_SN <= 232448, "SN tile exceeds the 227 KB shared-memory limit");
+// SS / RS: the three stored diagonal gradients of the centre plane, one TMA
+// box (PK x PJ x 1 x 3 fields of the work bundle), double-buffered by step.
+constexpr int NGB = 3;
+constexpr uint32_t GB_BYTES = NGB * PLANE * 8;
+constexpr int SMEM_BYTES_SS = NR * SLOT * 8 + 2 * NGB * PLANE * 8 + 128;
+static_assert(SMEM_BYTES_SS <= 232448, "SS tile exceeds the 227 KB shared-memory limit");
 static_assert(PLANE <= 2 * NT && BU1_N <= 2 * NT && BU2_N <= 2 * NT,
               "centre-plane buffer items: at most two per thread");
 
@@ -251,6 +257,51 @@ struct TiledLazyProvider {
   }
 };
 
+// SS / RS provider over the staged tile with FETCHed gradients staged too:
+// the centre plane's stored D(u0,x0), D(u1,x1), D(u2,x2) are a TMA box in
+// shared memory (gb*), the axis-0 neighbours of D(u1,x1), D(u2,x2) come from
+// register queues filled from the stored arrays, and the six off-diagonal
+// gradients at the point are loaded at step start.  Every value is read from
+// the work arrays (FETCH, plan.py:176-179); mixed terms apply the outer
+// stencil to the stored inner values exactly as codegen.py:111-113 does.
+template <bool INLINE_REST>
+struct TiledSSProvider {
+  const Coef& k;
+  const SAcc& a;
+  const double* q1;   // stored D(u1,x1) at this column, planes i-2..i+2
+  const double* q2;   // stored D(u2,x2)
+  const double* gb0;  // stored D(u0,x0), centre of the box (pitch PK)
+  const double* gb1;  // stored D(u1,x1)
+  const double* gb2;  // stored D(u2,x2)
+  const double* gv;   // off-diagonal D(u_q,x_a) at the point, [q*3+a]
+  template <int A_, int L, int OCC = 0>
+  __device__ __forceinline__ double g() const {
+    if constexpr (L >= S_U && L < S_U + 3) {
+      constexpr int q = L - S_U;
+      if constexpr (q == A_) return A_ == 0 ? gb0[0] : (A_ == 1 ? q1[2] : q2[2]);
+      else return gv[q * 3 + A_];
+    } else if constexpr (INLINE_REST) {
+      return eval_slot<A_, L>(k, a.rebased(zero_offset<OCC>()));
+    } else {
+      return eval_slot<A_, L>(k, a);
+    }
+  }
+  template <int J, int O, int OCC = 0>
+  __device__ __forceinline__ double x() const {
+    if constexpr (O == 0) {
+      const double* q = J == 1 ? q1 : q2;
+      return k.w1[0] * (q[3] - q[1]) + k.w2[0] * (q[4] - q[0]);
+    } else if constexpr (J == 0) {
+      constexpr int s = O == 1 ? PK : 1;
+      return k.w1[O] * (gb0[s] - gb0[-s]) + k.w2[O] * (gb0[2 * s] - gb0[-2 * s]);
+    } else if constexpr (J == 2) {
+      return k.w1[1] * (gb2[PK] - gb2[-PK]) + k.w2[1] * (gb2[2 * PK] - gb2[-2 * PK]);
+    } else {
+      return k.w1[2] * (gb1[1] - gb1[-1]) + k.w2[2] * (gb1[2] - gb1[-2]);
+    }
+  }
+};
+
 // BL work-array fill from the staged tile: the 54 plain/product derivatives
 // of one point into their arrays (plan.py:369-392).
 template <int A_, int L>
@@ -298,13 +349,17 @@ struct Segments {
 
 template <int V, int MODE, bool LAZY = true>
 __global__ void __launch_bounds__(NT, 1)
-    k_stage_tiled(const __grid_constant__ CUtensorMap tin, const double* __restrict__ work,
-                  const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
-                  int64_t total_steps, int wrap_mask, int i_lo, int nplanes, int aligned) {
+    k_stage_tiled(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tgw,
+                  const double* __restrict__ work, const double* saved, double* out, Coef k,
+                  Geom g, double coef, int ntk, int64_t total_steps, int wrap_mask, int i_lo,
+                  int nplanes, int aligned) {
   extern __shared__ __align__(128) double sm[];
   constexpr bool kBuf = (V == FDNS_SN);
-  double* bufs0 = sm + NR * SLOT;   // 2 x NBUF planes (SN only)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NR * SLOT + (kBuf ? 2 * NBUF * PLANE : 0));
+  constexpr bool kGB = (V == FDNS_SS || V == FDNS_RS) && MODE != 2;
+  double* bufs0 = sm + NR * SLOT;   // SN: 2 x NBUF buffer planes; SS/RS: 2 x NGB staged
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      sm + NR * SLOT + (kBuf ? 2 * NBUF * PLANE : (kGB ? 2 * NGB * PLANE : 0)));
+  uint64_t* gbars = bars + NR;      // SS/RS: the two gradient-box barriers
   const int tid = threadIdx.x;
   const int tk = tid % TK, tj = tid / TK;
   Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes,
@@ -314,9 +369,22 @@ __global__ void __launch_bounds__(NT, 1)
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < NR; ++s) mbar_init(&bars[s], 1);
+    if constexpr (kGB) { mbar_init(&gbars[0], 1); mbar_init(&gbars[1], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+
+  // SS/RS: staged gradient box of the centre plane of step `gs`
+  auto issue_gb = [&](int gs, int64_t tile, int plane) {
+    double* dst = bufs0 + (gs & 1) * NGB * PLANE;
+    mbar_expect_tx(&gbars[gs & 1], GB_BYTES);
+    tma_load_plane(dst, &tgw, &gbars[gs & 1], (int)(tile % ntk) * TK + g.h - 2,
+                   (int)(tile / ntk) * TJ + g.h - 2, plane + g.h);
+  };
+  if constexpr (kGB) {
+    if (tid == 0) issue_gb(0, S.beg / nplanes, i_lo + (int)(S.beg % nplanes));
+  }
+  int gs = 0;   // step counter of this CTA (gradient-box parity)
 
   // producer cursor (thread 0): stream position, current segment, position
   // within it
@@ -350,7 +418,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int toff = (tj + 2) * PK + (tk + 2);
     const int nsteps = (int)(se - x);
     double q1[5], q2[5];   // SN axis-0 queues
-    for (int t = 0; t < nsteps; ++t, ++w) {
+    for (int t = 0; t < nsteps; ++t, ++w, ++gs) {
       if (t == 0 && w > 0) {
         // segment change: the new window needs 5 fresh planes; refill the
         // ring once every thread is done with the previous segment's slots
@@ -404,6 +472,13 @@ __global__ void __launch_bounds__(NT, 1)
         if (issued < total_pos && issued < w + NR) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           while (issued < total_pos && issued < w + NR) issue_next();
+        }
+        if constexpr (kGB) {   // next step's centre gradient box
+          if (t + 1 < nsteps) {
+            issue_gb(gs + 1, x / nplanes, i_lo + (int)(x % nplanes) + t + 1);
+          } else if (se < S.end) {
+            issue_gb(gs + 1, se / nplanes, i_lo + (int)(se % nplanes));
+          }
         }
       }
       SAcc a;
@@ -470,7 +545,30 @@ __global__ void __launch_bounds__(NT, 1)
         // inactive (edge) threads read a valid clamped column; never written
         const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(min(jj, g.n1 - 1) + g.h) * g.s1 +
                           (min(kk, g.n2 - 1) + g.h);
-        SSProvider<SAcc, V == FDNS_RS> P(k, a, work, c, g.fs, g.s0, g.s1);
+        const double* w11 = work + 4 * g.fs + c;   // stored D(u1,x1)
+        const double* w22 = work + 8 * g.fs + c;   // stored D(u2,x2)
+        if (t == 0) {
+#pragma unroll
+          for (int d = 0; d < 5; ++d) {
+            q1[d] = __ldg(w11 + (d - 2) * g.s0);
+            q2[d] = __ldg(w22 + (d - 2) * g.s0);
+          }
+        } else {
+#pragma unroll
+          for (int d = 0; d < 4; ++d) { q1[d] = q1[d + 1]; q2[d] = q2[d + 1]; }
+          q1[4] = __ldg(w11 + 2 * g.s0);
+          q2[4] = __ldg(w22 + 2 * g.s0);
+        }
+        double gv[9];
+        gv[0 * 3 + 1] = __ldg(work + 1 * g.fs + c);
+        gv[0 * 3 + 2] = __ldg(work + 2 * g.fs + c);
+        gv[1 * 3 + 0] = __ldg(work + 3 * g.fs + c);
+        gv[1 * 3 + 2] = __ldg(work + 5 * g.fs + c);
+        gv[2 * 3 + 0] = __ldg(work + 6 * g.fs + c);
+        gv[2 * 3 + 1] = __ldg(work + 7 * g.fs + c);
+        mbar_wait(&gbars[gs & 1], (gs >> 1) & 1);
+        const double* gb = bufs0 + (gs & 1) * NGB * PLANE + toff;
+        const TiledSSProvider<V == FDNS_RS> P{k, a, q1, q2, gb, gb + PLANE, gb + 2 * PLANE, gv};
         residual_point<true>(k, P, r, R);
       }
       if (active) {
