@@ -408,7 +408,12 @@ __global__ void __launch_bounds__(NT, 1)
   if (tid == 0)
     while (issued < total_pos && issued < NR) issue_next();
 
-  int w = 0;   // stream position of the current window start
+  int w = 0;    // stream position of the current window start
+  int wsl = 0;  // w % NR, maintained incrementally (no per-step modulo)
+  auto slot_of = [&](int d) {  // ring slot of window position d (0..5)
+    const int x = wsl + d;
+    return x >= NR ? x - NR : x;
+  };
   for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) {
     const int64_t se = S.seg_end(x);
     const int64_t tile = x / nplanes;
@@ -418,7 +423,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int toff = (tj + 2) * PK + (tk + 2);
     const int nsteps = (int)(se - x);
     double q1[5], q2[5];   // SN axis-0 queues
-    for (int t = 0; t < nsteps; ++t, ++w, ++gs) {
+    for (int t = 0; t < nsteps; ++t, ++w, ++gs, wsl = (wsl + 1 == NR ? 0 : wsl + 1)) {
       if (t == 0 && w > 0) {
         // segment change: the new window needs 5 fresh planes; refill the
         // ring once every thread is done with the previous segment's slots
@@ -428,10 +433,15 @@ __global__ void __launch_bounds__(NT, 1)
           while (issued < total_pos && issued < w + NR) issue_next();
         }
       }
-      const int first = t == 0 ? w : w + 4;
-      for (int pp = first; pp <= w + 4; ++pp) {
-        mbar_wait(&bars[pp % NR], (pp / NR) & 1);
-        stage_arrival(k, sm + (pp % NR) * SLOT, tid, NT);
+      if (t == 0) {
+        for (int d = 0; d < 5; ++d) {
+          const int pp = w + d;
+          mbar_wait(&bars[slot_of(d)], (pp / NR) & 1);
+          stage_arrival(k, sm + slot_of(d) * SLOT, tid, NT);
+        }
+      } else {
+        mbar_wait(&bars[slot_of(4)], ((w + 4) / NR) & 1);
+        stage_arrival(k, sm + slot_of(4) * SLOT, tid, NT);
       }
       double* bufs = bufs0 + (w & 1) * NBUF * PLANE;
       if constexpr (kBuf) {
@@ -441,7 +451,7 @@ __global__ void __launch_bounds__(NT, 1)
         // positions tid and tid+NT of each buffer, predicated.
         const double* base[5];
 #pragma unroll
-        for (int d = 0; d < 5; ++d) base[d] = sm + ((w + d) % NR) * SLOT;
+        for (int d = 0; d < 5; ++d) base[d] = sm + slot_of(d) * SLOT;
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
           const int x0 = tid + m * NT;                       // D(u0,x0), whole box
@@ -483,7 +493,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
       SAcc a;
 #pragma unroll
-      for (int d = 0; d < 5; ++d) a.p[d] = sm + ((w + d) % NR) * SLOT + toff;
+      for (int d = 0; d < 5; ++d) a.p[d] = sm + slot_of(d) * SLOT + toff;
 
       if constexpr (kBuf) {
         // axis-0 queues of D(u1,x1), D(u2,x2) at this column
@@ -584,6 +594,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     w += 4;   // the segment's trailing positions
+    wsl = w % NR;
   }
 }
 
