@@ -493,3 +493,17 @@ def test_halo_width_and_box_lengths(variant, h):
     want = np.stack(npo.residual(F, h, w, CO))
     got = fd.assemble_residual(st, C, variant).interior_numpy()
     assert np.array_equal(got, want)
+
+
+def test_bench_variants_tables(tmp_path):
+    """The reference's bench harness semantics on the GPU (bench.py:51-88):
+    one record per (grid, plan), BL-normalised speedups, CSV files."""
+    from paper_1610_09146_b200 import benchtables as bt
+    recs = bt.bench_variants([(16, 16, 16)], ("BL", "SN", "SS"), iterations=2)
+    assert [r.plan for r in recs] == ["BL", "SN", "SS"]
+    assert all(r.loop_seconds > 0 and np.isfinite(r.final_ke) for r in recs)
+    kes = {r.final_ke for r in recs}
+    assert len(kes) == 1            # identical trajectories across variants
+    bt.write_bench_csv(recs, tmp_path / "bench.csv")
+    bt.write_speedup_csv(recs, tmp_path / "speedup.csv")
+    assert (tmp_path / "speedup.csv").read_text().startswith("Nx,Ny,Nz,BL,SN,SS")

@@ -169,3 +169,28 @@ def test_plan_introspection_matches_reference(built, golden_meta):
     for name in fd.PLAN_NAMES:
         assert fd.workarray_budget(fd.build_plan(name)) == \
             ref[name] - (1 if name == "BL" else 0)
+
+
+def test_bench_tables_formats(tmp_path):
+    """bench.csv / speedup.csv / scaling.csv in the reference's formats
+    (bench.py:108-126, 199-205)."""
+    from paper_1610_09146_b200 import benchtables as bt
+    assert bt.auto_dt((64, 64, 64)) == 3.385e-3
+    assert abs(bt.auto_dt((128,) * 3) - 3.385e-3 / 2) < 1e-18
+    recs = [bt.TimingRecord((64,) * 3, p, 1, 100, t)
+            for p, t in (("BL", 2.0), ("SN", 0.5), ("SS", 1.0))]
+    bt.write_bench_csv(recs, tmp_path / "bench.csv")
+    lines = (tmp_path / "bench.csv").read_text().splitlines()
+    assert lines[0] == "Nx,Ny,Nz,plan,workers,iterations,loop_seconds"
+    assert lines[2] == "64,64,64,SN,1,100,0.500000"
+    bt.write_speedup_csv(recs, tmp_path / "speedup.csv")
+    sp = (tmp_path / "speedup.csv").read_text().splitlines()
+    assert sp == ["Nx,Ny,Nz,BL,SN,SS", "64,64,64,1.0000,4.0000,2.0000"]
+    bench_lines = [{"n_gpus": n, "ms_per_step": 1.0 / n * 1.1 ** (n > 1),
+                    "steps": 10, "config": {"grid": [256, 256, 256]}}
+                   for n in (1, 2, 4, 8)]
+    sc = bt.scaling_records(bench_lines)
+    assert [r.ideal for r in sc] == [1.0, 0.5, 0.25, 0.125]
+    bt.write_scaling_csv(sc, tmp_path / "scaling.csv")
+    assert (tmp_path / "scaling.csv").read_text().splitlines()[0] == \
+        "workers,Nx,Ny,Nz,runtime,normalized,ideal"
