@@ -111,6 +111,11 @@ void fdns_set_kernel_path(int32_t path);
  * boundaries inside one CTA. */
 void fdns_set_tiled_grid(int32_t ctas);
 
+/* Programmatic dependent launch of the tiled stage kernels (default on):
+ * a stage's CTAs are dispatched as the previous stage's retire and wait in
+ * griddepcontrol.wait before any global access. */
+void fdns_set_pdl(int32_t enabled);
+
 /* Device reduction of the diagnostics of a state bundle (halos current):
  * out[0] = sum 0.5*rho*|u|^2, out[1] = sum 0.5*rho*|omega|^2, with rho from
  * `state` and the velocities (fields 5-7) from `prim_state` (NULL = state;

@@ -55,6 +55,7 @@ EXPORTS = {
                                _I, _I, ctypes.POINTER(Problem), _VP]),
     "fdns_set_kernel_path": (None, [_I]),
     "fdns_set_tiled_grid": (None, [_I]),
+    "fdns_set_pdl": (None, [_I]),
     "fdns_diag_partials_size": (_I, [ctypes.POINTER(Problem)]),
     "fdns_reduce_diag": (_I, [_VP, _VP, _VP, _VP, ctypes.POINTER(Problem),
                               _VP]),

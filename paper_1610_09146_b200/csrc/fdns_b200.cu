@@ -506,6 +506,26 @@ int num_sms() {
 // minimising the longest CTA in plane steps, a ramp costing ~2.5 steps
 // (measured: ~9 us per ramp vs ~3.4 us per step on B200).
 struct Launch { int64_t ctas; int aligned; };
+
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor in the stream drains; it executes
+// griddepcontrol.wait before any global memory access.
+bool g_pdl = true;
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 Launch pick_launch(int64_t tiles, int planes) {
   const int64_t total = tiles * planes;
   if (g_tiled_ctas > 0) return {std::min<int64_t>(g_tiled_ctas, total), 1};
@@ -544,8 +564,8 @@ int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
   const Launch L = pick_launch(ntk * ntj, nplanes);
-  tiled::k_stage_tiled<V, MODE, LAZY><<<(unsigned)L.ctas, tiled::NT, smem, s>>>(
-      m, mg, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes, L.aligned);
+  launch_pdl(tiled::k_stage_tiled<V, MODE, LAZY>, dim3((unsigned)L.ctas), dim3(tiled::NT), smem, s,
+             m, mg, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes, L.aligned);
   return 0;
 }
 
@@ -563,8 +583,8 @@ int launch_sn2(const CUtensorMap& m, const double* saved, double* out, const Coe
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
   const Launch L = pick_launch(ntk * ntj, nplanes);
-  sn2::k_stage_sn2<MODE><<<(unsigned)L.ctas, sn2::NT, sn2::SMEM_BYTES, s>>>(
-      m, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes, L.aligned);
+  launch_pdl(sn2::k_stage_sn2<MODE>, dim3((unsigned)L.ctas), dim3(sn2::NT), sn2::SMEM_BYTES, s,
+             m, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes, L.aligned);
   return 0;
 }
 
@@ -660,6 +680,8 @@ int64_t fdns_launch_count(void) { return g_launches.load(); }
 void fdns_set_kernel_path(int32_t path) { g_kernel_path = path; }
 
 void fdns_set_tiled_grid(int32_t ctas) { g_tiled_ctas = ctas; }
+
+void fdns_set_pdl(int32_t enabled) { g_pdl = enabled != 0; }
 
 int32_t fdns_workarray_count(int32_t variant) {
   switch (variant) {

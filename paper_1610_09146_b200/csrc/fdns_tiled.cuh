@@ -373,6 +373,11 @@ __global__ void __launch_bounds__(NT, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // Programmatic dependent launch: let the next stage's grid launch now (its
+  // CTAs take SMs as ours retire and run their prologue), and wait for the
+  // previous stage's writes before touching global memory.
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   // SS/RS: staged gradient box of the centre plane of step `gs`
   auto issue_gb = [&](int gs, int64_t tile, int plane) {
