@@ -507,3 +507,70 @@ def test_bench_variants_tables(tmp_path):
     bt.write_bench_csv(recs, tmp_path / "bench.csv")
     bt.write_speedup_csv(recs, tmp_path / "speedup.csv")
     assert (tmp_path / "speedup.csv").read_text().startswith("Nx,Ny,Nz,BL,SN,SS")
+
+
+# ------------------------------------------- time-loop contract (test_timeloop.py)
+def _quiescent(n=8):
+    shape = (n,) * 3
+    cons = np.stack([np.ones(shape), np.zeros(shape), np.zeros(shape),
+                     np.zeros(shape), np.full(shape, (1.0 / C.gM2) / C.gm1)])
+    return state_from_cons(grid_of(shape), cons)
+
+
+def test_quiescent_state_unchanged():
+    """test_timeloop.py:79-86."""
+    st = _quiescent()
+    before = host_cons(st)
+    fd.run(st, fd.RKScheme(dt=1e-2), fd.ResidualEvaluator(st.grid, C, "SS"), 2)
+    assert np.array_equal(host_cons(st), before)
+
+
+def test_zero_iterations():
+    """test_timeloop.py:88-97."""
+    st = _quiescent()
+    before = host_cons(st)
+    rep = fd.run(st, fd.RKScheme(dt=1e-2), fd.ResidualEvaluator(st.grid, C, "RA"), 0)
+    assert rep.iterations == 0 and rep.records == []
+    assert np.array_equal(host_cons(st), before)
+
+
+def test_save_state_snapshot():
+    """test_timeloop.py:99-105."""
+    g = grid_of((8,) * 3)
+    st = fd.taylor_green_init(g, C)
+    it = fd.IterationState(st)
+    it.save_state()
+    assert torch.equal(it.saved, st.bundle[:5])
+
+
+def test_timing_and_cadence():
+    """test_timeloop.py:138-149, 160-166: samples at iterations 0, 2, 4, 6;
+    loop time positive; run completes."""
+    g = grid_of((16,) * 3)
+    st = fd.taylor_green_init(g, C)
+    rho0 = fd.mean_density(st)
+    rep = fd.run(st, fd.RKScheme(dt=6.77e-3), fd.ResidualEvaluator(g, C, "SS"), 6,
+                 cadence=2, collect=fd.make_collector(g, rho0))
+    assert len(rep.records) == 4
+    assert rep.records[0].time == 0.0
+    assert rep.records[-1].time == pytest.approx(6 * 6.77e-3, rel=1e-12)
+    assert rep.loop_seconds > 0.0 and rep.completed
+
+
+def test_mass_conservation_short_run():
+    """test_timeloop.py:130-136: |mass drift| <= 1e-10 relative."""
+    g = grid_of((16,) * 3)
+    st = fd.taylor_green_init(g, C)
+    m0 = fd.reduce_sum(st.rho)
+    fd.run(st, fd.RKScheme(dt=6.77e-3), fd.ResidualEvaluator(g, C, "SS"), 20)
+    assert abs(fd.reduce_sum(st.rho) - m0) <= 1e-10 * abs(m0)
+
+
+def test_timeseries_csv_from_device_run(tmp_path):
+    """diagnostics.py:166-190 round trip of device-sampled records."""
+    g = grid_of((16,) * 3)
+    st = fd.taylor_green_init(g, C)
+    rep = fd.run(st, fd.RKScheme(dt=6.77e-3), fd.ResidualEvaluator(g, C, "SN"), 4,
+                 cadence=2, collect=fd.make_collector(g, fd.mean_density(st)))
+    fd.write_timeseries(rep.records, tmp_path / "ts.csv")
+    assert fd.read_timeseries(tmp_path / "ts.csv") == rep.records
