@@ -427,8 +427,7 @@ __global__ void __launch_bounds__(NT, 1)
     const bool active = jj < g.n1 && kk < g.n2;
     const int toff = (tj + 2) * PK + (tk + 2);
     const int nsteps = (int)(se - x);
-    double q1[5], q2[5];   // axis-0 queues (SN: computed; SS/RS: stored values)
-    double q1n = 0.0, q2n = 0.0;   // SS/RS: next leading values, prefetched
+    double q1[5], q2[5];   // SN axis-0 queues
     for (int t = 0; t < nsteps; ++t, ++w, ++gs, wsl = (wsl + 1 == NR ? 0 : wsl + 1)) {
       if (t == 0 && w > 0) {
         // segment change: the new window needs 5 fresh planes; refill the
@@ -572,12 +571,8 @@ __global__ void __launch_bounds__(NT, 1)
         } else {
 #pragma unroll
           for (int d = 0; d < 4; ++d) { q1[d] = q1[d + 1]; q2[d] = q2[d + 1]; }
-          q1[4] = q1n;
-          q2[4] = q2n;
-        }
-        if (t + 1 < nsteps) {   // next step's leading plane, one step ahead
-          q1n = __ldg(w11 + 3 * g.s0);
-          q2n = __ldg(w22 + 3 * g.s0);
+          q1[4] = __ldg(w11 + 2 * g.s0);
+          q2[4] = __ldg(w22 + 2 * g.s0);
         }
         double gv[9];
         gv[0 * 3 + 1] = __ldg(work + 1 * g.fs + c);
