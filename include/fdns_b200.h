@@ -116,6 +116,11 @@ void fdns_set_tiled_grid(int32_t ctas);
  * griddepcontrol.wait before any global access. */
 void fdns_set_pdl(int32_t enabled);
 
+/* Debug timeline of the tiled stage kernels: enable (1) / disable (0) the
+ * per-CTA %globaltimer stamps (entry, prologue done, first window ready,
+ * exit; 4 per CTA) and copy up to n of them to host memory `out`. */
+int32_t fdns_debug_trace(int32_t enable, uint64_t* out, int32_t n);
+
 /* Device reduction of the diagnostics of a state bundle (halos current):
  * out[0] = sum 0.5*rho*|u|^2, out[1] = sum 0.5*rho*|omega|^2, with rho from
  * `state` and the velocities (fields 5-7) from `prim_state` (NULL = state;

@@ -56,6 +56,7 @@ EXPORTS = {
     "fdns_set_kernel_path": (None, [_I]),
     "fdns_set_tiled_grid": (None, [_I]),
     "fdns_set_pdl": (None, [_I]),
+    "fdns_debug_trace": (_I, [_I, ctypes.POINTER(ctypes.c_uint64), _I]),
     "fdns_diag_partials_size": (_I, [ctypes.POINTER(Problem)]),
     "fdns_reduce_diag": (_I, [_VP, _VP, _VP, _VP, ctypes.POINTER(Problem),
                               _VP]),

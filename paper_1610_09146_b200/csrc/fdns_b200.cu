@@ -683,6 +683,18 @@ void fdns_set_tiled_grid(int32_t ctas) { g_tiled_ctas = ctas; }
 
 void fdns_set_pdl(int32_t enabled) { g_pdl = enabled != 0; }
 
+int32_t fdns_debug_trace(int32_t enable, uint64_t* out, int32_t n) {
+  int on = enable;
+  if (cudaMemcpyToSymbol(tiled::g_trace_on, &on, sizeof(int)) != cudaSuccess)
+    return fail("trace flag", cudaGetLastError());
+  if (out && n > 0) {
+    const int m = std::min(n, tiled::TRACE_CTAS * tiled::TRACE_PTS);
+    if (cudaMemcpyFromSymbol(out, tiled::g_trace, m * sizeof(uint64_t)) != cudaSuccess)
+      return fail("trace copy", cudaGetLastError());
+  }
+  return 0;
+}
+
 int32_t fdns_workarray_count(int32_t variant) {
   switch (variant) {
     case FDNS_BL: return N_SLOTS;

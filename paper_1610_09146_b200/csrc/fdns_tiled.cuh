@@ -26,6 +26,19 @@ namespace fdns {
 namespace tiled {
 
 constexpr int TK = 32, TJ = 8, NT = TK * TJ;
+
+// Optional per-CTA timeline (debug): %globaltimer stamps at kernel entry,
+// after the prologue, when the first window is ready, and at exit.
+constexpr int TRACE_CTAS = 1024, TRACE_PTS = 4;
+__device__ unsigned long long g_trace[TRACE_CTAS * TRACE_PTS];
+__constant__ int g_trace_on;
+__device__ __forceinline__ void trace(int pt) {
+  if (g_trace_on && threadIdx.x == 0 && blockIdx.x < TRACE_CTAS) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[blockIdx.x * TRACE_PTS + pt] = t;
+  }
+}
 constexpr int PK = TK + 4, PJ = TJ + 4;
 constexpr int PLANE = PK * PJ;          // doubles per field per plane slot
 constexpr int SLOT = NFIELDS * PLANE;   // doubles per plane slot
@@ -365,6 +378,7 @@ __global__ void __launch_bounds__(NT, 1)
   Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes,
                                                    aligned);
   if (S.beg >= S.end) return;
+  trace(0);
 
   if (tid == 0) {
 #pragma unroll
@@ -378,6 +392,7 @@ __global__ void __launch_bounds__(NT, 1)
   // previous stage's writes before touching global memory.
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  trace(1);
 
   // SS/RS: staged gradient box of the centre plane of step `gs`
   auto issue_gb = [&](int gs, int64_t tile, int plane) {
@@ -483,6 +498,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
       __syncthreads();
+      if (w == 0) trace(2);
       if (tid == 0) {
         if (issued < total_pos && issued < w + NR) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -601,6 +617,7 @@ __global__ void __launch_bounds__(NT, 1)
     w += 4;   // the segment's trailing positions
     wsl = w % NR;
   }
+  trace(3);
 }
 
 }  // namespace tiled

@@ -1,0 +1,45 @@
+"""Per-CTA timeline of one SN stage (debug stamps): prologue, first-window
+ramp, steady part, spread of exit times.
+
+    python tools/trace_stage.py [n0 n1 n2]
+"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_1610_09146_b200 as fd
+from paper_1610_09146_b200 import _lib
+
+torch.cuda.set_device(0)
+lib = _lib.load()
+npts = tuple(int(x) for x in sys.argv[1:4]) if len(sys.argv) > 3 else (64, 64, 64)
+variant = sys.argv[4] if len(sys.argv) > 4 else "SN"
+g = fd.make_grid(npts, (2 * np.pi,) * 3)
+c = fd.PhysicalConstants()
+s = fd.taylor_green_init(g, c)
+ev = fd.ResidualEvaluator(g, c, variant)
+Y, Z = ev.workspace()
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for cold in (True, False):
+    for _ in range(3):
+        ev.stage(s.bundle, s.bundle, Y, 1e-3)
+    torch.cuda.synchronize()
+    _lib.check(lib.fdns_debug_trace(1, None, 0))
+    if cold:
+        lib.fdns_l2_flush(_lib.ptr(flush), flush.numel(), _lib.stream_handle())
+    ev.stage(s.bundle, s.bundle, Y, 1e-3)
+    torch.cuda.synchronize()
+    buf = (ctypes.c_uint64 * (1024 * 4))()
+    _lib.check(lib.fdns_debug_trace(0, buf, 1024 * 4))
+    t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 4).astype(np.float64)
+    t = t[t[:, 0] > 0]
+    t0 = t[:, 0].min()
+    rel = (t - t0) / 1e3
+    print(f"{variant} {npts} {'cold' if cold else 'warm'} L2: {len(t)} CTAs")
+    for k, name in enumerate(("entry", "prologue", "window ready", "exit")):
+        print(f"  {name:13s} min {rel[:, k].min():7.2f}  median {np.median(rel[:, k]):7.2f}"
+              f"  max {rel[:, k].max():7.2f} us")
