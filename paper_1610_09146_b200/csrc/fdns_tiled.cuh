@@ -36,6 +36,11 @@ __device__ __forceinline__ void trace(int pt) {
   if (g_trace_on && threadIdx.x == 0 && blockIdx.x < TRACE_CTAS) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (pt == 0) {   // entry stamp carries the SM id in its top bits
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      t = (t & 0x0000FFFFFFFFFFFFull) | ((unsigned long long)smid << 48);
+    }
     g_trace[blockIdx.x * TRACE_PTS + pt] = t;
   }
 }

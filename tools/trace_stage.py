@@ -35,11 +35,26 @@ for cold in (True, False):
     torch.cuda.synchronize()
     buf = (ctypes.c_uint64 * (1024 * 4))()
     _lib.check(lib.fdns_debug_trace(0, buf, 1024 * 4))
-    t = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 4).astype(np.float64)
-    t = t[t[:, 0] > 0]
+    raw = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 4).copy()
+    ncta = int((raw[:, 0] > 0).sum())
+    raw = raw[:ncta]
+    smid = (raw[:, 0] >> np.uint64(48)).astype(int)
+    raw[:, 0] &= np.uint64(0x0000FFFFFFFFFFFF)
+    mask48 = np.uint64(0x0000FFFFFFFFFFFF)
+    t = (raw & mask48).astype(np.float64)
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3
     print(f"{variant} {npts} {'cold' if cold else 'warm'} L2: {len(t)} CTAs")
     for k, name in enumerate(("entry", "prologue", "window ready", "exit")):
         print(f"  {name:13s} min {rel[:, k].min():7.2f}  median {np.median(rel[:, k]):7.2f}"
               f"  max {rel[:, k].max():7.2f} us")
+    dur = rel[:, 3] - rel[:, 2]
+    order = np.argsort(-dur)
+    print("  slowest CTAs (cta, smid, steady us):",
+          [(int(i), int(smid[i]), round(float(dur[i]), 1)) for i in order[:8]])
+    print("  fastest CTAs:", [(int(i), int(smid[i]), round(float(dur[i]), 1)) for i in order[-5:]])
+    # SM parity / die split
+    for name, sel in (("even smid", smid % 2 == 0), ("odd smid", smid % 2 == 1),
+                      ("smid<74", smid < 74), ("smid>=74", smid >= 74)):
+        if sel.any():
+            print(f"  {name:9s}: mean steady {dur[sel].mean():8.1f} us  max {dur[sel].max():8.1f}")
