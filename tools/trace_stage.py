@@ -18,6 +18,7 @@ torch.cuda.set_device(0)
 lib = _lib.load()
 npts = tuple(int(x) for x in sys.argv[1:4]) if len(sys.argv) > 3 else (64, 64, 64)
 variant = sys.argv[4] if len(sys.argv) > 4 else "SN"
+wrap = int(sys.argv[5]) if len(sys.argv) > 5 else 7
 g = fd.make_grid(npts, (2 * np.pi,) * 3)
 c = fd.PhysicalConstants()
 s = fd.taylor_green_init(g, c)
@@ -31,7 +32,9 @@ for cold in (True, False):
     _lib.check(lib.fdns_debug_trace(1, None, 0))
     if cold:
         lib.fdns_l2_flush(_lib.ptr(flush), flush.numel(), _lib.stream_handle())
-    ev.stage(s.bundle, s.bundle, Y, 1e-3)
+    _lib.check(lib.fdns_stage(ev.plan.variant_id, _lib.ptr(s.bundle), _lib.ptr(s.bundle),
+                              _lib.ptr(Y), ev.work_ptr, 1e-3, wrap, ev.problem,
+                              _lib.stream_handle()))
     torch.cuda.synchronize()
     buf = (ctypes.c_uint64 * (1024 * 4))()
     _lib.check(lib.fdns_debug_trace(0, buf, 1024 * 4))
