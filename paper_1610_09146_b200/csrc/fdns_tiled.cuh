@@ -112,13 +112,16 @@ struct SAcc {
   }
 };
 
-// Write the 10 (MODE 1) or 5 (MODE 0) output values of interior point
-// (i, j, k) to its location and to every periodic ghost image on the axes
-// of wrap_mask (mesh.py:118-139 semantics: ghost = value at the wrapped
-// coordinates).
+// Write the NOUT output values of interior point (i, j, k) to its location
+// and to every periodic ghost image on the axes of wrap_mask (mesh.py:118-139
+// semantics: ghost = value at the wrapped coordinates).  When every wrapped
+// axis has n >= 2h a coordinate has at most one image, and the (up to 7)
+// image stores are explicit predicated stores -- no dynamically indexed
+// arrays, so no local memory on the edge warps.  Tiny axes (n < 2h, where a
+// point can have an image on both sides) take the general loop.
 template <int NOUT>
-__device__ __forceinline__ void emit(double* out, const Geom& g, int i, int j, int k,
-                                     const double* val, int wrap_mask) {
+__device__ __noinline__ void emit_general(double* out, const Geom& g, int i, int j, int k,
+                                          const double* val, int wrap_mask) {
   const int h = g.h;
   int ci[3], cj[3], ck[3], ni = 1, nj = 1, nk = 1;
   ci[0] = i + h; cj[0] = j + h; ck[0] = k + h;
@@ -134,21 +137,49 @@ __device__ __forceinline__ void emit(double* out, const Geom& g, int i, int j, i
     if (k < h) ck[nk++] = k + h + g.n2;
     if (k >= g.n2 - h) ck[nk++] = k + h - g.n2;
   }
-  {
-    const int64_t c = ci[0] * g.s0 + cj[0] * g.s1 + ck[0];
+  for (int a = 0; a < ni; ++a)
+    for (int b = 0; b < nj; ++b)
+      for (int d = 0; d < nk; ++d) {
+        const int64_t c = ci[a] * g.s0 + cj[b] * g.s1 + ck[d];
+        for (int f = 0; f < NOUT; ++f) out[f * g.fs + c] = val[f];
+      }
+}
+
+template <int NOUT>
+__device__ __forceinline__ void emit_at(double* out, const Geom& g, int64_t c, const double* val) {
 #pragma unroll
-    for (int f = 0; f < NOUT; ++f) out[f * g.fs + c] = val[f];
-  }
-  if (ni * nj * nk > 1) {
-    for (int a = 0; a < ni; ++a)
-      for (int b = 0; b < nj; ++b)
-        for (int d = 0; d < nk; ++d) {
-          if ((a | b | d) == 0) continue;
-          const int64_t c = ci[a] * g.s0 + cj[b] * g.s1 + ck[d];
+  for (int f = 0; f < NOUT; ++f) out[f * g.fs + c] = val[f];
+}
+
+template <int NOUT>
+__device__ __forceinline__ void emit(double* out, const Geom& g, int i, int j, int k,
+                                     const double* val, int wrap_mask) {
+  const int h = g.h;
+  const int64_t ci = i + h, cj = j + h, ck = k + h;
+  emit_at<NOUT>(out, g, ci * g.s0 + cj * g.s1 + ck, val);
+  if (wrap_mask == 0) return;
+  const bool small = ((wrap_mask & 1) && g.n0 < 2 * h) || ((wrap_mask & 2) && g.n1 < 2 * h) ||
+                     ((wrap_mask & 4) && g.n2 < 2 * h);
+  if (small) {
+    // the general path rewrites the interior value too (same bits)
+    double v[NOUT];
 #pragma unroll
-          for (int f = 0; f < NOUT; ++f) out[f * g.fs + c] = val[f];
-        }
+    for (int f = 0; f < NOUT; ++f) v[f] = val[f];
+    emit_general<NOUT>(out, g, i, j, k, v, wrap_mask);
+    return;
   }
+  // at most one image per axis: its padded coordinate, or -1
+  const int64_t gi = !(wrap_mask & 1) ? -1 : (i < h ? ci + g.n0 : (i >= g.n0 - h ? ci - g.n0 : -1));
+  const int64_t gj = !(wrap_mask & 2) ? -1 : (j < h ? cj + g.n1 : (j >= g.n1 - h ? cj - g.n1 : -1));
+  const int64_t gk = !(wrap_mask & 4) ? -1 : (k < h ? ck + g.n2 : (k >= g.n2 - h ? ck - g.n2 : -1));
+  if (gi < 0 && gj < 0 && gk < 0) return;
+  if (gi >= 0) emit_at<NOUT>(out, g, gi * g.s0 + cj * g.s1 + ck, val);
+  if (gj >= 0) emit_at<NOUT>(out, g, ci * g.s0 + gj * g.s1 + ck, val);
+  if (gk >= 0) emit_at<NOUT>(out, g, ci * g.s0 + cj * g.s1 + gk, val);
+  if (gi >= 0 && gj >= 0) emit_at<NOUT>(out, g, gi * g.s0 + gj * g.s1 + ck, val);
+  if (gi >= 0 && gk >= 0) emit_at<NOUT>(out, g, gi * g.s0 + cj * g.s1 + gk, val);
+  if (gj >= 0 && gk >= 0) emit_at<NOUT>(out, g, ci * g.s0 + gj * g.s1 + gk, val);
+  if (gi >= 0 && gj >= 0 && gk >= 0) emit_at<NOUT>(out, g, gi * g.s0 + gj * g.s1 + gk, val);
 }
 
 // Arrival conversion of one staged plane slot (all PLANE points of the box):
