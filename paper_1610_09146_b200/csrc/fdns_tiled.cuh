@@ -120,7 +120,7 @@ struct SAcc {
 // arrays, so no local memory on the edge warps.  Tiny axes (n < 2h, where a
 // point can have an image on both sides) take the general loop.
 template <int NOUT>
-__device__ __noinline__ void emit_general(double* out, const Geom& g, int i, int j, int k,
+__device__ __forceinline__ void emit_general(double* out, const Geom& g, int i, int j, int k,
                                           const double* val, int wrap_mask) {
   const int h = g.h;
   int ci[3], cj[3], ck[3], ni = 1, nj = 1, nk = 1;
