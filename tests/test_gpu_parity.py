@@ -574,3 +574,23 @@ def test_timeseries_csv_from_device_run(tmp_path):
                  cadence=2, collect=fd.make_collector(g, fd.mean_density(st)))
     fd.write_timeseries(rep.records, tmp_path / "ts.csv")
     assert fd.read_timeseries(tmp_path / "ts.csv") == rep.records
+
+
+@pytest.mark.parametrize("variant", ["SN", "SS", "BL"])
+def test_host_stepper_matches_run(variant):
+    """hostio.HostStepper (pinned host buffers, pipelined copies) advances
+    the host arrays exactly as run() advances the device state."""
+    from paper_1610_09146_b200.hostio import HostStepper
+    g = grid_of((24, 20, 16))
+    F = npo.manufactured((24, 20, 16), CO)
+    ref = state_from_cons(g, npo.interior(F[:5], 2))
+    fd.run(ref, fd.RKScheme(dt=2e-3), fd.ResidualEvaluator(g, C, variant), 3)
+    st = state_from_cons(g, npo.interior(F[:5], 2))
+    host = HostStepper.pinned_buffers(g)
+    host.copy_(st.bundle[:5].cpu())
+    stepper = HostStepper(st, fd.ResidualEvaluator(g, C, variant), fd.RKScheme(dt=2e-3))
+    for _ in range(3):
+        stepper.step(host)
+    stepper.wait()
+    torch.cuda.synchronize()
+    assert np.array_equal(host.numpy(), ref.bundle[:5].cpu().numpy())
