@@ -47,6 +47,7 @@ struct Geom {
 // the compiler (used by LOCAL/FETCH providers).
 struct GAcc {
   static constexpr bool kInternalEnergy = false;
+  static constexpr bool kMaskTaps = false;   // INLINE occurrences rebase (L1 hits)
   const double* __restrict__ b;
   int64_t c, s0, s1, fs;
   __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
@@ -70,6 +71,60 @@ __device__ __forceinline__ int zero_offset() {
   return g_zero_offset[OCC % N_ZERO_OFFSETS];
 }
 
+// Register-level variant (shared-memory accessors with FDNS_RA_OPAQUE=1, the
+// default; global-memory point kernels keep the rebased addresses, which
+// measured faster there -- the shared loads spill): taps are loaded
+// once (the compiler may share loads between occurrences), and each
+// occurrence XORs the high word of selected taps with its own
+// constant-bank zero.  The result is bit-identical to the tap, yet opaque to the
+// compiler, so every occurrence's arithmetic is still recomputed -- at the
+// cost of about one integer instruction per tap instead of one
+// shared-memory load.
+#ifndef FDNS_RA_OPAQUE
+#define FDNS_RA_OPAQUE 1
+#endif
+__constant__ int g_zero_word[N_ZERO_OFFSETS];
+
+template <int OCC>
+__device__ __forceinline__ double opaque(double x) {
+  return __hiloint2double(__double2hiint(x) ^ g_zero_word[OCC % N_ZERO_OFFSETS],
+                          __double2loint(x));
+}
+
+// Accessor of one INLINE occurrence: `v` reads a tap plainly, `m` reads it
+// masked.  The stencils mask one operand of every first-level operation
+// (ep1, ep2 of a first derivative; the centre, +1, +2 taps of a second
+// derivative; the first factor of every product and of rho*e), which
+// already makes every value of the occurrence distinct to the compiler.
+template <class Acc, int OCC>
+struct OpaqueAcc {
+  static constexpr bool kInternalEnergy = Acc::kInternalEnergy;
+  const Acc& a;
+  __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
+    return a.v(f, di, dj, dk);
+  }
+  __device__ __forceinline__ double m(int f, int di, int dj, int dk) const {
+    return opaque<OCC>(a.v(f, di, dj, dk));
+  }
+};
+
+template <class A> struct is_opaque { static constexpr bool value = false; };
+template <class A, int O> struct is_opaque<OpaqueAcc<A, O>> { static constexpr bool value = true; };
+
+// A tap read, masked when M and the accessor is an occurrence view.
+template <bool M, class A>
+__device__ __forceinline__ double tap(const A& a, int f, int di, int dj, int dk) {
+  if constexpr (M && is_opaque<A>::value) return a.m(f, di, dj, dk);
+  else return a.v(f, di, dj, dk);
+}
+
+// The accessor one INLINE occurrence evaluates through.
+template <int OCC, class Acc>
+__device__ __forceinline__ auto occurrence_view(const Acc& a) {
+  if constexpr (FDNS_RA_OPAQUE && Acc::kMaskTaps) return OpaqueAcc<Acc, OCC>{a};
+  else return a.rebased(zero_offset<OCC>());
+}
+
 // ---------------------------------------------------------------------------
 // Point expressions of the term list (terms.py:39, :158-174)
 // ---------------------------------------------------------------------------
@@ -83,27 +138,28 @@ template <int AX> struct Off {
 // tiles hold it precomputed in place of rhoE (kInternalEnergy): the same
 // per-point expression, evaluated once per staged point instead of once per
 // stencil tap, so the bits are identical.
-template <class A>
+template <bool M = false, class A>
 __device__ __forceinline__ double rhoe_at(const A& a, int di, int dj, int dk) {
   if constexpr (A::kInternalEnergy) {
-    return a.v(RHOE_F, di, dj, dk);
-  } else {
+    return tap<M>(a, RHOE_F, di, dj, dk);
+  } else {   // arithmetic: every product masked, so no occurrence shares
+             // any part of it
     return a.v(RHOE_F, di, dj, dk) -
-           0.5 * (a.v(RU0, di, dj, dk) * a.v(U0, di, dj, dk) +
-                  a.v(RU1, di, dj, dk) * a.v(U1, di, dj, dk) +
-                  a.v(RU2, di, dj, dk) * a.v(U2, di, dj, dk));
+           0.5 * (tap<true>(a, RU0, di, dj, dk) * a.v(U0, di, dj, dk) +
+                  tap<true>(a, RU1, di, dj, dk) * a.v(U1, di, dj, dk) +
+                  tap<true>(a, RU2, di, dj, dk) * a.v(U2, di, dj, dk));
   }
 }
 
 // Expression kinds differentiated by the stencils.
 enum Ex : int { E_FIELD = 0, E_PROD, E_RHOE, E_RHOEU };
 
-template <int EX, int F, int G, class A>
+template <int EX, int F, int G, bool M = false, class A>
 __device__ __forceinline__ double ex_at(const A& a, int di, int dj, int dk) {
-  if constexpr (EX == E_FIELD) return a.v(F, di, dj, dk);
-  else if constexpr (EX == E_PROD) return a.v(F, di, dj, dk) * a.v(G, di, dj, dk);
-  else if constexpr (EX == E_RHOE) return rhoe_at(a, di, dj, dk);
-  else return rhoe_at(a, di, dj, dk) * a.v(G, di, dj, dk);
+  if constexpr (EX == E_FIELD) return tap<M>(a, F, di, dj, dk);
+  else if constexpr (EX == E_PROD) return tap<true>(a, F, di, dj, dk) * a.v(G, di, dj, dk);
+  else if constexpr (EX == E_RHOE) return rhoe_at<M>(a, di, dj, dk);
+  else return rhoe_at<true>(a, di, dj, dk) * a.v(G, di, dj, dk);
 }
 
 // First derivative along AX of expression EX at centre+(bi,bj,bk):
@@ -113,9 +169,9 @@ __device__ __forceinline__ double d1(const Coef& k, const A& a, int bi = 0,
                                      int bj = 0, int bk = 0) {
   int i1, j1, k1;
   Off<AX>::at(1, i1, j1, k1);
-  const double ep1 = ex_at<EX, F, G>(a, bi + i1, bj + j1, bk + k1);
+  const double ep1 = ex_at<EX, F, G, true>(a, bi + i1, bj + j1, bk + k1);
   const double em1 = ex_at<EX, F, G>(a, bi - i1, bj - j1, bk - k1);
-  const double ep2 = ex_at<EX, F, G>(a, bi + 2 * i1, bj + 2 * j1, bk + 2 * k1);
+  const double ep2 = ex_at<EX, F, G, true>(a, bi + 2 * i1, bj + 2 * j1, bk + 2 * k1);
   const double em2 = ex_at<EX, F, G>(a, bi - 2 * i1, bj - 2 * j1, bk - 2 * k1);
   return k.w1[AX] * (ep1 - em1) + k.w2[AX] * (ep2 - em2);
 }
@@ -125,9 +181,9 @@ template <int AX, int F, class A>
 __device__ __forceinline__ double d2(const Coef& k, const A& a) {
   int i1, j1, k1;
   Off<AX>::at(1, i1, j1, k1);
-  return k.s0[AX] * a.v(F, 0, 0, 0) +
-         k.s1[AX] * (a.v(F, i1, j1, k1) + a.v(F, -i1, -j1, -k1)) +
-         k.s2[AX] * (a.v(F, 2 * i1, 2 * j1, 2 * k1) + a.v(F, -2 * i1, -2 * j1, -2 * k1));
+  return k.s0[AX] * tap<true>(a, F, 0, 0, 0) +
+         k.s1[AX] * (tap<true>(a, F, i1, j1, k1) + a.v(F, -i1, -j1, -k1)) +
+         k.s2[AX] * (tap<true>(a, F, 2 * i1, 2 * j1, 2 * k1) + a.v(F, -2 * i1, -2 * j1, -2 * k1));
 }
 
 // Mixed DD(u_J, x_O, x_J): outer first derivative along O of the inner first
@@ -198,10 +254,10 @@ struct InlineProvider {
   const Acc& a;
   __device__ InlineProvider(const Coef& k_, const Acc& a_) : k(k_), a(a_) {}
   template <int A_, int L, int OCC = 0> __device__ __forceinline__ double g() const {
-    return eval_slot<A_, L>(k, a.rebased(zero_offset<OCC>()));
+    return eval_slot<A_, L>(k, occurrence_view<OCC>(a));
   }
   template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const {
-    return dd<O, J>(k, a.rebased(zero_offset<OCC>()));
+    return dd<O, J>(k, occurrence_view<OCC>(a));
   }
 };
 
@@ -255,7 +311,7 @@ struct SSProvider {
       : k(k_), a(a_), ws(ws_), c(c_), fs(fs_) { st[0] = s0; st[1] = s1; st[2] = 1; }
   template <int A_, int L, int OCC = 0> __device__ __forceinline__ double g() const {
     if constexpr (L >= S_U && L < S_U + 3) return __ldg(ws + ((L - S_U) * 3 + A_) * fs + c);
-    else if constexpr (INLINE_REST) return eval_slot<A_, L>(k, a.rebased(zero_offset<OCC>()));
+    else if constexpr (INLINE_REST) return eval_slot<A_, L>(k, occurrence_view<OCC>(a));
     else return eval_slot<A_, L>(k, a);
   }
   template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const {

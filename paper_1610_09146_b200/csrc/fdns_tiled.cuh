@@ -100,6 +100,7 @@ __device__ __forceinline__ void tma_load_plane(double* dst, const CUtensorMap* m
 // already offset to this thread's (j, k) column and field 0.
 struct SAcc {
   static constexpr bool kInternalEnergy = true;   // field RHOE_F holds rho*e
+  static constexpr bool kMaskTaps = true;         // INLINE occurrences mask taps
   const double* p[5];
   __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
     return p[di + 2][f * PLANE + dj * PK + dk];
@@ -330,7 +331,7 @@ struct TiledSSProvider {
       if constexpr (q == A_) return A_ == 0 ? gb0[0] : (A_ == 1 ? q1[2] : q2[2]);
       else return gv[q * 3 + A_];
     } else if constexpr (INLINE_REST) {
-      return eval_slot<A_, L>(k, a.rebased(zero_offset<OCC>()));
+      return eval_slot<A_, L>(k, occurrence_view<OCC>(a));
     } else {
       return eval_slot<A_, L>(k, a);
     }
@@ -431,11 +432,13 @@ __global__ void __launch_bounds__(NT, 1)
   trace(1);
 
   // SS/RS: staged gradient box of the centre plane of step `gs`
-  auto issue_gb = [&](int gs, int64_t tile, int plane) {
+  auto issue_gb_tile = [&](int gs, int k0, int j0, int plane) {
     double* dst = bufs0 + (gs & 1) * NGB * PLANE;
     mbar_expect_tx(&gbars[gs & 1], GB_BYTES);
-    tma_load_plane(dst, &tgw, &gbars[gs & 1], (int)(tile % ntk) * TK + g.h - 2,
-                   (int)(tile / ntk) * TJ + g.h - 2, plane + g.h);
+    tma_load_plane(dst, &tgw, &gbars[gs & 1], k0 + g.h - 2, j0 + g.h - 2, plane + g.h);
+  };
+  auto issue_gb = [&](int gs, int64_t tile, int plane) {
+    issue_gb_tile(gs, (int)(tile % ntk) * TK, (int)(tile / ntk) * TJ, plane);
   };
   if constexpr (kGB) {
     if (tid == 0) issue_gb(0, S.beg / nplanes, i_lo + (int)(S.beg % nplanes));
@@ -444,20 +447,30 @@ __global__ void __launch_bounds__(NT, 1)
 
   // producer cursor (thread 0): stream position, current segment, position
   // within it
+  // (box coordinates are recomputed only when the cursor enters a segment:
+  // no 64-bit division per issued plane)
   int64_t p_seg = S.beg;
   int p_r = 0;
   int issued = 0;
-  auto issue_next = [&]() {
-    const int64_t se = S.seg_end(p_seg);
-    const int len = (int)(se - p_seg) + 4;
+  int p_len = 0, p_c0 = 0, p_c1 = 0, p_plane = 0, p_slot = 0;
+  auto enter_segment = [&]() {
     const int64_t tile = p_seg / nplanes;
-    const int plane = i_lo + (int)(p_seg % nplanes) - 2 + p_r;
-    const int slot = issued % NR;
-    mbar_expect_tx(&bars[slot], LOAD_BYTES);
-    tma_load_plane(sm + slot * SLOT, &tin, &bars[slot], (int)(tile % ntk) * TK + g.h - 2,
-                   (int)(tile / ntk) * TJ + g.h - 2, plane + g.h);
+    p_len = (int)(S.seg_end(p_seg) - p_seg) + 4;
+    p_c0 = (int)(tile % ntk) * TK + g.h - 2;
+    p_c1 = (int)(tile / ntk) * TJ + g.h - 2;
+    p_plane = i_lo + (int)(p_seg % nplanes) - 2 + g.h;
+  };
+  if (tid == 0) enter_segment();
+  auto issue_next = [&]() {
+    mbar_expect_tx(&bars[p_slot], LOAD_BYTES);
+    tma_load_plane(sm + p_slot * SLOT, &tin, &bars[p_slot], p_c0, p_c1, p_plane + p_r);
     ++issued;
-    if (++p_r == len) { p_r = 0; p_seg = se; }
+    p_slot = p_slot + 1 == NR ? 0 : p_slot + 1;
+    if (++p_r == p_len) {
+      p_r = 0;
+      p_seg = S.seg_end(p_seg);
+      if (p_seg < S.end) enter_segment();
+    }
   };
   int total_pos = 0;
   for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) total_pos += (int)(S.seg_end(x) - x) + 4;
@@ -478,6 +491,7 @@ __global__ void __launch_bounds__(NT, 1)
     const bool active = jj < g.n1 && kk < g.n2;
     const int toff = (tj + 2) * PK + (tk + 2);
     const int nsteps = (int)(se - x);
+    const int i_seg = i_lo + (int)(x % nplanes);   // axis-0 index of step 0
     double q1[5], q2[5];   // SN axis-0 queues
     for (int t = 0; t < nsteps; ++t, ++w, ++gs, wsl = (wsl + 1 == NR ? 0 : wsl + 1)) {
       if (t == 0 && w > 0) {
@@ -542,7 +556,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
         if constexpr (kGB) {   // next step's centre gradient box
           if (t + 1 < nsteps) {
-            issue_gb(gs + 1, x / nplanes, i_lo + (int)(x % nplanes) + t + 1);
+            issue_gb_tile(gs + 1, k0, j0, i_seg + t + 1);
           } else if (se < S.end) {
             issue_gb(gs + 1, se / nplanes, i_lo + (int)(se % nplanes));
           }
@@ -572,7 +586,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
 
-      const int i = i_lo + (int)(x % nplanes) + t;
+      const int i = i_seg + t;
       if constexpr (MODE == 2) {   // BL fill: derivative arrays only
         if (active) {
           const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(jj + g.h) * g.s1 + (kk + g.h);
