@@ -118,7 +118,10 @@ void fdns_set_pdl(int32_t enabled);
 
 /* Debug timeline of the tiled stage kernels: enable (1) / disable (0) the
  * per-CTA %globaltimer stamps (entry, prologue done, first window ready,
- * exit; 4 per CTA) and copy up to n of them to host memory `out`. */
+ * exit; 4 per CTA) and copy up to n of them to host memory `out`.
+ * enable = 2 starts a launch log (every CTA of every launch appends its four
+ * stamps and blockIdx | smid << 16); enable = 3 stops it and copies
+ * [count, count x 5 words] to `out`. */
 int32_t fdns_debug_trace(int32_t enable, uint64_t* out, int32_t n);
 
 /* Device reduction of the diagnostics of a state bundle (halos current):
@@ -144,6 +147,14 @@ int32_t fdns_fp64_probe(double* scratch, int32_t iters, double* out_count,
 
 /* L2 flush helper for timing hygiene: writes `bytes` of `buf`. */
 int32_t fdns_l2_flush(void* buf, int64_t bytes, void* stream);
+
+/* Copy `bytes` between two UVA addresses with an SM kernel (`ctas` CTAs,
+ * <= 0: 4 per SM): device memory or pinned (mapped) host memory on either
+ * side, 16-byte aligned.  The host-buffer stepping path (hostio.py) uses it
+ * for the upload of the reference-layout host fields (the role of the
+ * numpy arrays the reference passes to ResidualEvaluator.evaluate,
+ * plan.py:394-416). */
+int32_t fdns_copy_sm(void* dst, const void* src, int64_t bytes, int32_t ctas, void* stream);
 
 #ifdef __cplusplus
 }

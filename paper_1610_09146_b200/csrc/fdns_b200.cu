@@ -426,6 +426,14 @@ __global__ void k_l2_flush(uint4* buf, int64_t n, uint32_t v) {
     buf[t] = make_uint4(v, v + 1, v + 2, v + 3);
 }
 
+// SM-driven copy between any two UVA addresses (device memory or pinned,
+// mapped host memory): many 16-byte requests in flight from every SM.
+__global__ void k_copy16(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    dst[t] = src[t];
+}
+
 inline dim3 point_grid(const Geom& g, dim3 blk) {
   return dim3((g.n2 + blk.x - 1) / blk.x, (g.n1 + blk.y - 1) / blk.y, g.n0);
 }
@@ -687,6 +695,25 @@ int32_t fdns_debug_trace(int32_t enable, uint64_t* out, int32_t n) {
   int on = enable;
   if (cudaMemcpyToSymbol(tiled::g_trace_on, &on, sizeof(int)) != cudaSuccess)
     return fail("trace flag", cudaGetLastError());
+  if (enable == 2) {   // log mode: start a fresh launch log
+    unsigned zero = 0;
+    if (cudaMemcpyToSymbol(tiled::g_trace_n, &zero, sizeof(zero)) != cudaSuccess)
+      return fail("trace log reset", cudaGetLastError());
+  }
+  if (out && n > 0 && enable == 3) {   // read the launch log: [count, records...]
+    unsigned cnt = 0;
+    if (cudaMemcpyFromSymbol(&cnt, tiled::g_trace_n, sizeof(cnt)) != cudaSuccess)
+      return fail("trace log count", cudaGetLastError());
+    cnt = std::min<unsigned>(cnt, tiled::TRACE_LOG_N);
+    out[0] = cnt;
+    const int m = std::min<int64_t>(n - 1, (int64_t)cnt * tiled::TRACE_LOG_W);
+    if (m > 0 && cudaMemcpyFromSymbol(out + 1, tiled::g_trace_log, m * sizeof(uint64_t)) !=
+                     cudaSuccess)
+      return fail("trace log copy", cudaGetLastError());
+    on = 0;
+    cudaMemcpyToSymbol(tiled::g_trace_on, &on, sizeof(int));
+    return 0;
+  }
   if (out && n > 0) {
     const int m = std::min(n, tiled::TRACE_CTAS * tiled::TRACE_PTS);
     if (cudaMemcpyFromSymbol(out, tiled::g_trace, m * sizeof(uint64_t)) != cudaSuccess)
@@ -810,6 +837,17 @@ int32_t fdns_l2_flush(void* buf, int64_t bytes, void* stream) {
   static uint32_t v = 1;
   k_l2_flush<<<148 * 8, 256, 0, (cudaStream_t)stream>>>((uint4*)buf, n, v++);
   return check_launch("l2 flush");
+}
+
+int32_t fdns_copy_sm(void* dst, const void* src, int64_t bytes, int32_t ctas, void* stream) {
+  if (((uintptr_t)dst | (uintptr_t)src | (uintptr_t)bytes) & 15)
+    return fail("fdns_copy_sm: pointers and size must be 16-byte aligned");
+  if (bytes <= 0) return 0;
+  const int64_t n = bytes / 16;
+  const int grid = ctas > 0 ? ctas : 148 * 4;
+  k_copy16<<<grid, 256, 0, (cudaStream_t)stream>>>((uint4*)dst, (const uint4*)src, n);
+  count();
+  return check_launch("sm copy");
 }
 
 }  // extern "C"

@@ -32,16 +32,30 @@ constexpr int TK = 32, TJ = 8, NT = TK * TJ;
 constexpr int TRACE_CTAS = 1024, TRACE_PTS = 4;
 __device__ unsigned long long g_trace[TRACE_CTAS * TRACE_PTS];
 __constant__ int g_trace_on;
+// Log mode (g_trace_on == 2): every CTA of every launch also appends its
+// four stamps plus (blockIdx | smid << 16) to g_trace_log, so a sequence of
+// launches (a whole RK step) can be reconstructed.
+constexpr int TRACE_LOG_N = 8192, TRACE_LOG_W = 5;
+__device__ unsigned long long g_trace_log[TRACE_LOG_N * TRACE_LOG_W];
+__device__ unsigned int g_trace_n;
 __device__ __forceinline__ void trace(int pt) {
   if (g_trace_on && threadIdx.x == 0 && blockIdx.x < TRACE_CTAS) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (pt == 0) {   // entry stamp carries the SM id in its top bits
-      unsigned smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (pt == 0)   // entry stamp carries the SM id in its top bits
       t = (t & 0x0000FFFFFFFFFFFFull) | ((unsigned long long)smid << 48);
-    }
     g_trace[blockIdx.x * TRACE_PTS + pt] = t;
+    if (pt == TRACE_PTS - 1 && g_trace_on == 2) {
+      const unsigned idx = atomicAdd(&g_trace_n, 1u);
+      if (idx < TRACE_LOG_N) {
+        unsigned long long* r = g_trace_log + (size_t)idx * TRACE_LOG_W;
+        for (int q = 0; q < TRACE_PTS; ++q)
+          r[q] = g_trace[blockIdx.x * TRACE_PTS + q] & 0x0000FFFFFFFFFFFFull;
+        r[TRACE_PTS] = blockIdx.x | ((unsigned long long)smid << 16);
+      }
+    }
   }
 }
 constexpr int PK = TK + 4, PJ = TJ + 4;

@@ -576,21 +576,55 @@ def test_timeseries_csv_from_device_run(tmp_path):
     assert fd.read_timeseries(tmp_path / "ts.csv") == rep.records
 
 
-@pytest.mark.parametrize("variant", ["SN", "SS", "BL"])
-def test_host_stepper_matches_run(variant):
-    """hostio.HostStepper (pinned host buffers, pipelined copies) advances
-    the host arrays exactly as run() advances the device state."""
+@pytest.mark.parametrize("variant,graphs,chunks", [
+    ("SN", True, 4), ("SS", True, 3), ("BL", True, 1), ("SN", False, 4), ("RA", False, 2)])
+def test_host_stepper_matches_run(variant, graphs, chunks):
+    """hostio.HostStepper (pinned host buffers, chunked copies pipelined
+    across steps, graph-captured or eager) advances the host arrays exactly
+    as run() advances the device state, including across a wait() in the
+    middle of a run."""
     from paper_1610_09146_b200.hostio import HostStepper
     g = grid_of((24, 20, 16))
     F = npo.manufactured((24, 20, 16), CO)
     ref = state_from_cons(g, npo.interior(F[:5], 2))
+    fd.run(ref, fd.RKScheme(dt=2e-3), fd.ResidualEvaluator(g, C, variant), 2)
+    mid = ref.bundle[:5].cpu().numpy().copy()
     fd.run(ref, fd.RKScheme(dt=2e-3), fd.ResidualEvaluator(g, C, variant), 3)
     st = state_from_cons(g, npo.interior(F[:5], 2))
     host = HostStepper.pinned_buffers(g)
     host.copy_(st.bundle[:5].cpu())
-    stepper = HostStepper(st, fd.ResidualEvaluator(g, C, variant), fd.RKScheme(dt=2e-3))
+    stepper = HostStepper(st, fd.ResidualEvaluator(g, C, variant), fd.RKScheme(dt=2e-3),
+                          host, chunks=chunks, graphs=graphs)
+    for _ in range(2):
+        stepper.step()
+    stepper.wait()
+    torch.cuda.synchronize()
+    assert np.array_equal(host.numpy(), mid)
     for _ in range(3):
-        stepper.step(host)
+        stepper.step()
+    stepper.wait()
+    torch.cuda.synchronize()
+    assert np.array_equal(host.numpy(), ref.bundle[:5].cpu().numpy())
+    assert stepper.it.iteration == 5
+
+
+def test_host_stepper_sees_host_edits():
+    """A modification of the host buffer between wait() and the next step()
+    is what the next step advances (the upload is real)."""
+    from paper_1610_09146_b200.hostio import HostStepper
+    g = grid_of((16, 16, 16))
+    F = npo.manufactured((16, 16, 16), CO)
+    st = state_from_cons(g, npo.interior(F[:5], 2))
+    host = HostStepper.pinned_buffers(g)
+    host.copy_(st.bundle[:5].cpu())
+    stepper = HostStepper(st, fd.ResidualEvaluator(g, C, "SN"), fd.RKScheme(dt=2e-3), host)
+    stepper.step()
+    stepper.wait()
+    torch.cuda.synchronize()
+    ref = state_from_cons(g, 1.0001 * npo.interior(F[:5], 2))
+    host.copy_(ref.bundle[:5].cpu())
+    fd.run(ref, fd.RKScheme(dt=2e-3), fd.ResidualEvaluator(g, C, "SN"), 1)
+    stepper.step()
     stepper.wait()
     torch.cuda.synchronize()
     assert np.array_equal(host.numpy(), ref.bundle[:5].cpu().numpy())
