@@ -5,8 +5,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -496,6 +498,25 @@ bool plane_map(CUtensorMap* m, const double* base, const Geom& g) {
   return r == CUDA_SUCCESS;
 }
 
+// Saved-state tile of one plane (TK x TJ x 1 x 5 conservative fields), the
+// box the stage kernel's L2 prefetch requests.
+bool saved_map(CUtensorMap* m, const double* saved, const Geom& g) {
+  const int64_t P2 = g.n2 + 2 * g.h, P1 = g.n1 + 2 * g.h, P0 = g.n0 + 2 * g.h;
+  if (P2 % 2 != 0 || g.h % 2 != 0) return false;
+  if (reinterpret_cast<uintptr_t>(saved) % 16 != 0) return false;
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)P2, (cuuint64_t)P1, (cuuint64_t)P0, 5};
+  cuuint64_t strides[3] = {(cuuint64_t)(P2 * 8), (cuuint64_t)(P1 * P2 * 8),
+                           (cuuint64_t)(g.fs * 8)};
+  cuuint32_t box[4] = {tiled::TK, tiled::TJ, 1, 5};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(saved), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 int g_num_sms = 0;
 int num_sms() {
   if (!g_num_sms) {
@@ -508,11 +529,10 @@ int num_sms() {
 }
 
 // Persistent grid: one CTA per SM with at least ~4 plane steps each, split
-// either into equal contiguous ranges in tile-major order (a CTA may span
-// two tiles and then pays the pipeline ramp twice) or tile-aligned (one ramp
-// per CTA, but ranges quantised per tile).  Pick the split and CTA count
-// minimising the longest CTA in plane steps, a ramp costing ~2.5 steps
-// (measured: ~9 us per ramp vs ~3.4 us per step on B200).
+// contiguous, tile-aligned or balanced (Segments::partition).  Pick the split
+// and CTA count minimising the longest CTA, in plane steps plus ~1.25 steps
+// per extra segment (mid-range ramp; measured ~3.3 us vs ~3.0 us per step at
+// 64^3), evaluated exactly over the CTAs of each candidate and cached.
 struct Launch { int64_t ctas; int aligned; };
 
 // Launch with programmatic stream serialization (PDL): the kernel may start
@@ -534,33 +554,59 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
+double split_cost(int64_t G, int64_t tiles, int planes, int mode) {
+  const int64_t total = tiles * planes;
+  const double Rm = tiled::RAMP_MID_Q / 4.0;
+  double worst = 0;
+  for (int64_t b = 0; b < G; ++b) {
+    const tiled::Segments S = tiled::Segments::partition(b, G, total, planes, mode);
+    if (S.beg >= S.end) continue;
+    int segs = 0;
+    for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) ++segs;
+    worst = std::max(worst, (double)(S.end - S.beg) + Rm * (segs - 1));
+  }
+  return worst;
+}
+
 Launch pick_launch(int64_t tiles, int planes) {
   const int64_t total = tiles * planes;
-  if (g_tiled_ctas > 0) return {std::min<int64_t>(g_tiled_ctas, total), 1};
-  const double R = 2.5;
+  if (g_tiled_ctas > 0) return {std::min<int64_t>(g_tiled_ctas, total), tiled::SPLIT_ALIGNED};
+  static std::map<std::pair<int64_t, int>, Launch> cache;
+  const auto key = std::make_pair(tiles, planes);
+  const auto hit = cache.find(key);
+  if (hit != cache.end()) return hit->second;
   const int64_t G0 = std::max<int64_t>(1, std::min<int64_t>(num_sms(), total / 4));
-  const int64_t len0 = (total + G0 - 1) / G0;
-  // ranges shorter than a tile may straddle a tile boundary
-  Launch best{G0, 0};
-  double best_cost = len0 + R * (len0 < planes && planes % len0 ? 2 : 1);
+  Launch best{G0, tiled::SPLIT_CONTIGUOUS};
+  double best_cost = split_cost(G0, tiles, planes, tiled::SPLIT_CONTIGUOUS);
+  const double cb = split_cost(G0, tiles, planes, tiled::SPLIT_BALANCED);
+  if (cb < best_cost - 1e-9) { best_cost = cb; best = {G0, tiled::SPLIT_BALANCED}; }
   for (int64_t G = tiles; G <= G0; ++G) {
-    const int64_t mmin = G / tiles;
-    const double cost = (planes + mmin - 1) / mmin + R;
-    if (cost < best_cost - 1e-9) { best_cost = cost; best = {G, 1}; }
+    const double c = split_cost(G, tiles, planes, tiled::SPLIT_ALIGNED);
+    if (c < best_cost - 1e-9) { best_cost = c; best = {G, tiled::SPLIT_ALIGNED}; }
   }
+  cache[key] = best;
   return best;
 }
 
+// A/B switch for experiments: FDNS_NO_SAVED_PREFETCH=1 disables the L2
+// prefetch of the saved state.
+const bool g_prefetch_saved = std::getenv("FDNS_NO_SAVED_PREFETCH") == nullptr;
+
 template <int V, int MODE, bool LAZY = true>
-int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const double* work,
+int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, double* out,
+                   const double* work,
                    const Coef& k, const Geom& g, double coef, int wrap, int i_lo, int i_hi,
                    cudaStream_t s) {
   constexpr bool gb = (V == FDNS_SS || V == FDNS_RS) && MODE != 2;
   constexpr int smem = V == FDNS_SN ? tiled::SMEM_BYTES_SN
                                     : (gb ? tiled::SMEM_BYTES_SS : tiled::SMEM_BYTES);
-  CUtensorMap mg = m;
+  CUtensorMap mg = m, ms = m;
   if constexpr (gb)
     if (!grad_map(&mg, work, g)) return fail("gradient tensor map");
+  // saved state != stage input (RK stages 2 and 3): prefetch it into L2
+  int pf = 0;
+  if constexpr (MODE == 1)
+    pf = (g_prefetch_saved && saved != in && saved_map(&ms, saved, g)) ? 1 : 0;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tiled::k_stage_tiled<V, MODE, LAZY>,
@@ -573,7 +619,8 @@ int launch_tiled_v(const CUtensorMap& m, const double* saved, double* out, const
   const int64_t total = (int64_t)ntk * ntj * nplanes;
   const Launch L = pick_launch(ntk * ntj, nplanes);
   launch_pdl(tiled::k_stage_tiled<V, MODE, LAZY>, dim3((unsigned)L.ctas), dim3(tiled::NT), smem, s,
-             m, mg, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes, L.aligned);
+             m, mg, ms, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes,
+             L.aligned, pf);
   return 0;
 }
 
@@ -604,15 +651,15 @@ int launch_residual(int variant, const double* in, const double* saved, double* 
   CUtensorMap m;
   if (variant != FDNS_BL && g_kernel_path != 1 && plane_map(&m, in, g)) {
     switch (variant) {
-      case FDNS_RA: launch_tiled_v<FDNS_RA, MODE>(m, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
-      case FDNS_RS: launch_tiled_v<FDNS_RS, MODE>(m, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
+      case FDNS_RA: launch_tiled_v<FDNS_RA, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
+      case FDNS_RS: launch_tiled_v<FDNS_RS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
       case FDNS_SN:
         if (g_kernel_path == 3) launch_sn2<MODE>(m, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
         else if (g_kernel_path == 4)
-          launch_tiled_v<FDNS_SN, MODE, false>(m, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
-        else launch_tiled_v<FDNS_SN, MODE>(m, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
+          launch_tiled_v<FDNS_SN, MODE, false>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
+        else launch_tiled_v<FDNS_SN, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
         break;
-      case FDNS_SS: launch_tiled_v<FDNS_SS, MODE>(m, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
+      case FDNS_SS: launch_tiled_v<FDNS_SS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
       default: return fail("unknown variant");
     }
     count();

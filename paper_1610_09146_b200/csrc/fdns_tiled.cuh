@@ -110,6 +110,16 @@ __device__ __forceinline__ void tma_load_plane(double* dst, const CUtensorMap* m
       : "memory");
 }
 
+// L2 prefetch of a tensor box (no shared memory, no barrier): used for the
+// saved-state tile of a plane a few steps before its epilogue reads it.
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(0)
+      : "memory");
+}
+
 // Shared-memory accessor: p[d] is the plane slot for axis-0 offset d-2,
 // already offset to this thread's (j, k) column and field 0.
 struct SAcc {
@@ -380,22 +390,34 @@ __device__ __forceinline__ void fill_slots(const Coef& k, const SAcc& a, double*
 // range as <= a few segments (one per tile touched).  The TMA producer
 // (thread 0) streams the planes of all segments back to back through the
 // ring, prefetching across segment boundaries.
+// Partition modes of the (tile, plane) steps of one launch over G CTAs.
+enum SplitMode : int { SPLIT_CONTIGUOUS = 0, SPLIT_ALIGNED = 1, SPLIT_BALANCED = 2 };
+// Ramp of a segment that starts inside a CTA's range (ring refill, five
+// planes converted, queues rebuilt), in quarter plane steps (measured
+// ~3.3 us vs ~3.0 us per step at 64^3).
+constexpr int RAMP_MID_Q = 5;
+
 struct Segments {
   int64_t beg, end;   // [beg, end) in tile-major (tile * nplanes + plane) order
   int n0;             // planes per tile in this launch
-  __device__ __forceinline__ int64_t seg_end(int64_t x) const {
+  __host__ __device__ __forceinline__ int64_t seg_end(int64_t x) const {
     const int64_t tile_end = (x / n0 + 1) * (int64_t)n0;
     return tile_end < end ? tile_end : end;
   }
-  // CTA b of G over `total` = tiles * planes steps.  `aligned` (needs at
-  // least as many CTAs as tiles): split tile-aligned (each tile gets floor or ceil of
-  // G/tiles CTAs, each CTA one contiguous plane range of one tile: one
-  // pipeline ramp per CTA); otherwise equal contiguous ranges in tile-major
-  // order (a CTA may span tiles; its ramps amortise over many planes).
-  static __device__ __forceinline__ Segments partition(int64_t b, int64_t G, int64_t total,
-                                                       int planes, int aligned) {
+  // CTA b of G over `total` = tiles * planes steps.
+  //  SPLIT_ALIGNED (needs G >= tiles): each tile gets floor or ceil of
+  //    G/tiles CTAs, each CTA one contiguous plane range of one tile (one
+  //    pipeline ramp per CTA, ranges quantised per tile);
+  //  SPLIT_CONTIGUOUS: equal contiguous ranges in tile-major order (a CTA may
+  //    span tiles and pays a ramp per tile);
+  //  SPLIT_BALANCED: contiguous ranges of equal cost, a tile counting its
+  //    planes plus one mid-range ramp (RAMP_MID_Q), so a CTA whose range
+  //    contains a tile start gets correspondingly fewer planes.
+  static __host__ __device__ __forceinline__ Segments partition(int64_t b, int64_t G,
+                                                                int64_t total, int planes,
+                                                                int mode) {
     const int64_t tiles = total / planes;
-    if (aligned && G >= tiles) {
+    if (mode == SPLIT_ALIGNED && G >= tiles) {
       const int64_t base = G / tiles, rem = G % tiles;
       int64_t t, r, m;
       if (b < rem * (base + 1)) {
@@ -407,6 +429,20 @@ struct Segments {
       const int64_t p0 = r * planes / m, p1 = (r + 1) * planes / m;
       return Segments{t * planes + p0, t * planes + p1, planes};
     }
+    if (mode == SPLIT_BALANCED) {
+      const int64_t unit = 4 * (int64_t)planes + RAMP_MID_Q;   // quarter steps per tile
+      const int64_t V = tiles * unit;
+      auto cut = [&](int64_t bb) -> int64_t {
+        if (bb >= G) return total;
+        const int64_t v = bb * V / G;
+        const int64_t t = v / unit;
+        const int64_t off = v - t * unit - RAMP_MID_Q;
+        int64_t p = off > 0 ? (off + 2) / 4 : 0;
+        if (p > planes) p = planes;
+        return t * planes + p;
+      };
+      return Segments{cut(b), cut(b + 1), planes};
+    }
     return Segments{b * total / G, (b + 1) * total / G, planes};
   }
 };
@@ -414,9 +450,10 @@ struct Segments {
 template <int V, int MODE, bool LAZY = true>
 __global__ void __launch_bounds__(NT, 1)
     k_stage_tiled(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tgw,
-                  const double* __restrict__ work, const double* saved, double* out, Coef k,
-                  Geom g, double coef, int ntk, int64_t total_steps, int wrap_mask, int i_lo,
-                  int nplanes, int aligned) {
+                  const __grid_constant__ CUtensorMap tsv, const double* __restrict__ work,
+                  const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
+                  int64_t total_steps, int wrap_mask, int i_lo, int nplanes, int split,
+                  int pf_saved) {
   extern __shared__ __align__(128) double sm[];
   constexpr bool kBuf = (V == FDNS_SN);
   constexpr bool kGB = (V == FDNS_SS || V == FDNS_RS) && MODE != 2;
@@ -426,8 +463,7 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* gbars = bars + NR;      // SS/RS: the two gradient-box barriers
   const int tid = threadIdx.x;
   const int tk = tid % TK, tj = tid / TK;
-  Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes,
-                                                   aligned);
+  Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes, split);
   if (S.beg >= S.end) return;
   trace(0);
 
@@ -478,6 +514,11 @@ __global__ void __launch_bounds__(NT, 1)
   auto issue_next = [&]() {
     mbar_expect_tx(&bars[p_slot], LOAD_BYTES);
     tma_load_plane(sm + p_slot * SLOT, &tin, &bars[p_slot], p_c0, p_c1, p_plane + p_r);
+    // saved state of this plane (a centre plane of the segment) into L2,
+    // ~NR steps before the epilogue loads it: when it is not the stage
+    // input it would otherwise come from DRAM at full latency
+    if (MODE == 1 && pf_saved && p_r >= 2 && p_r < p_len - 2)
+      tma_prefetch_l2(&tsv, p_c0 + 2, p_c1 + 2, p_plane + p_r);
     ++issued;
     p_slot = p_slot + 1 == NR ? 0 : p_slot + 1;
     if (++p_r == p_len) {

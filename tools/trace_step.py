@@ -66,6 +66,9 @@ print(f"{variant} {n}^3, {steps} graph steps, event time {e0.elapsed_time(e1) * 
 # new launch begins where stamp 1 passes the running max exit
 order = np.argsort(rel[:, 1])
 rel = rel[order]
+meta = rec[order, 4]
+smid_all = ((meta >> np.uint64(16)) & np.uint64(0xFFFF)).astype(int)
+cta_all = (meta & np.uint64(0xFFFF)).astype(int)
 launch = np.zeros(cnt, dtype=int)
 li, mx = 0, -1.0
 for i in range(cnt):
@@ -86,3 +89,13 @@ for L in range(launch.max() + 1):
     ramp = r[:, 2] - r[:, 1]
     print(f"          ramp (wait-done->ready) med {np.median(ramp):5.2f} max {ramp.max():5.2f}; "
           f"steady med {np.median(steady):6.2f} max {steady.max():6.2f} us")
+    sm = smid_all[launch == L]
+    ct = cta_all[launch == L]
+    for name, sel in (("smid<74", sm < 74), ("smid>=74", sm >= 74), ("even", sm % 2 == 0),
+                      ("odd", sm % 2 == 1)):
+        if sel.any():
+            print(f"          {name:9s} steady mean {steady[sel].mean():7.2f}", end="")
+    print()
+    o = np.argsort(-steady)[:6]
+    print("          slowest (cta, smid, steady):",
+          [(int(ct[i]), int(sm[i]), round(float(steady[i]), 1)) for i in o])
