@@ -479,6 +479,25 @@ bool grad_map(CUtensorMap* m, const double* work, const Geom& g) {
   return r == CUDA_SUCCESS;
 }
 
+// The nine stored gradients of one plane's tile columns (TK x TJ x 1 x 9),
+// the box the SS/RS stage kernel prefetches into L2.
+bool grad_prefetch_map(CUtensorMap* m, const double* work, const Geom& g) {
+  const int64_t P2 = g.n2 + 2 * g.h, P1 = g.n1 + 2 * g.h, P0 = g.n0 + 2 * g.h;
+  if (P2 % 2 != 0 || g.h % 2 != 0) return false;
+  if (reinterpret_cast<uintptr_t>(work) % 16 != 0) return false;
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)P2, (cuuint64_t)P1, (cuuint64_t)P0, 9};
+  cuuint64_t strides[3] = {(cuuint64_t)(P2 * 8), (cuuint64_t)(P1 * P2 * 8),
+                           (cuuint64_t)(g.fs * 8)};
+  cuuint32_t box[4] = {tiled::TK, tiled::TJ, 1, 9};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(work), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool plane_map(CUtensorMap* m, const double* base, const Geom& g) {
   const int64_t P2 = g.n2 + 2 * g.h, P1 = g.n1 + 2 * g.h, P0 = g.n0 + 2 * g.h;
   // 16-byte rows, and an even innermost box start (k0 + h - 2): an odd one
@@ -600,9 +619,10 @@ int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, 
   constexpr bool gb = (V == FDNS_SS || V == FDNS_RS) && MODE != 2;
   constexpr int smem = V == FDNS_SN ? tiled::SMEM_BYTES_SN
                                     : (gb ? tiled::SMEM_BYTES_SS : tiled::SMEM_BYTES);
-  CUtensorMap mg = m, ms = m;
+  CUtensorMap mg = m, ms = m, mp = m;
   if constexpr (gb)
-    if (!grad_map(&mg, work, g)) return fail("gradient tensor map");
+    if (!grad_map(&mg, work, g) || !grad_prefetch_map(&mp, work, g))
+      return fail("gradient tensor map");
   // saved state != stage input (RK stages 2 and 3): prefetch it into L2
   int pf = 0;
   if constexpr (MODE == 1)
@@ -619,7 +639,7 @@ int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, 
   const int64_t total = (int64_t)ntk * ntj * nplanes;
   const Launch L = pick_launch(ntk * ntj, nplanes);
   launch_pdl(tiled::k_stage_tiled<V, MODE, LAZY>, dim3((unsigned)L.ctas), dim3(tiled::NT), smem, s,
-             m, mg, ms, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes,
+             m, mg, ms, mp, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes,
              L.aligned, pf);
   return 0;
 }

@@ -450,7 +450,8 @@ struct Segments {
 template <int V, int MODE, bool LAZY = true>
 __global__ void __launch_bounds__(NT, 1)
     k_stage_tiled(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tgw,
-                  const __grid_constant__ CUtensorMap tsv, const double* __restrict__ work,
+                  const __grid_constant__ CUtensorMap tsv, const __grid_constant__ CUtensorMap tgp,
+                  const double* __restrict__ work,
                   const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
                   int64_t total_steps, int wrap_mask, int i_lo, int nplanes, int split,
                   int pf_saved) {
@@ -519,6 +520,9 @@ __global__ void __launch_bounds__(NT, 1)
     // input it would otherwise come from DRAM at full latency
     if (MODE == 1 && pf_saved && p_r >= 2 && p_r < p_len - 2)
       tma_prefetch_l2(&tsv, p_c0 + 2, p_c1 + 2, p_plane + p_r);
+    // SS/RS: the nine stored gradients of this plane's tile columns (the
+    // off-diagonal loads at the centre and the axis-0 queue loads) into L2
+    if constexpr (kGB) tma_prefetch_l2(&tgp, p_c0 + 2, p_c1 + 2, p_plane + p_r);
     ++issued;
     p_slot = p_slot + 1 == NR ? 0 : p_slot + 1;
     if (++p_r == p_len) {
