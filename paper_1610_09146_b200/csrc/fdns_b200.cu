@@ -11,6 +11,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <tuple>
+#include <vector>
 
 #include "../../include/fdns_b200.h"
 #include "fdns_math.cuh"
@@ -552,8 +554,6 @@ int num_sms() {
 // and CTA count minimising the longest CTA, in plane steps plus ~1.25 steps
 // per extra segment (mid-range ramp; measured ~3.3 us vs ~3.0 us per step at
 // 64^3), evaluated exactly over the CTAs of each candidate and cached.
-struct Launch { int64_t ctas; int aligned; };
-
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // while its predecessor in the stream drains; it executes
 // griddepcontrol.wait before any global memory access.
@@ -573,37 +573,127 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
-double split_cost(int64_t G, int64_t tiles, int planes, int mode) {
-  const int64_t total = tiles * planes;
+// Cost model of a CTA's range: plane steps weighted by the tile's periodic
+// image writes (edge tiles store each point's images too and finish later:
+// measured +9% per step for a tile on a k edge, +8% on a j edge, at
+// 256^3), plus the mid-range ramp of every extra segment.
+// The image stores cost about the same time per point in every variant, so
+// the relative weight shrinks with the variant's time per point (SS/RS
+// ~1.05-1.1x SN).  For RA (1.45x) the weighted split measured no better
+// than the uniform ones (-0.7% at 256^3 and 512^3), so RA keeps weight 1.
+struct TileCost {
+  int ntk, ntj;
+  bool kw, jw;   // images written along axis 2 / axis 1
+  double scale;  // SN = 1
+  double weight(int64_t tile) const {
+    const int kt = (int)(tile % ntk), jt = (int)(tile / ntk);
+    return 1.0 + ((kw && (kt == 0 || kt == ntk - 1)) ? 0.09 * scale : 0.0) +
+           ((jw && (jt == 0 || jt == ntj - 1)) ? 0.08 * scale : 0.0);
+  }
+};
+#ifndef FDNS_EDGE_SCALE
+#define FDNS_EDGE_SCALE 1.0
+#endif
+inline double edge_scale(int variant) {
+  switch (variant) {
+    case FDNS_RA: return 0.0;
+    case FDNS_SS: return FDNS_EDGE_SCALE / 1.05;
+    case FDNS_RS: return FDNS_EDGE_SCALE / 1.1;
+    default: return FDNS_EDGE_SCALE;
+  }
+}
+
+double split_cost(int64_t G, const TileCost& tc, int planes, int mode,
+                  const int64_t* cuts = nullptr) {
+  const int64_t total = (int64_t)tc.ntk * tc.ntj * planes;
   const double Rm = tiled::RAMP_MID_Q / 4.0;
   double worst = 0;
   for (int64_t b = 0; b < G; ++b) {
-    const tiled::Segments S = tiled::Segments::partition(b, G, total, planes, mode);
+    const tiled::Segments S = tiled::Segments::partition(b, G, total, planes, mode, cuts);
     if (S.beg >= S.end) continue;
-    int segs = 0;
-    for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) ++segs;
-    worst = std::max(worst, (double)(S.end - S.beg) + Rm * (segs - 1));
+    double c = -Rm;
+    for (int64_t x = S.beg; x < S.end; x = S.seg_end(x))
+      c += (double)(S.seg_end(x) - x) * tc.weight(x / planes) + Rm;
+    worst = std::max(worst, c);
   }
   return worst;
 }
 
-Launch pick_launch(int64_t tiles, int planes) {
+// Cut points of G contiguous ranges of equal weighted cost in tile-major
+// order (each tile: its plane steps times its weight, plus one mid-range
+// ramp).
+std::vector<int64_t> table_cuts(int64_t G, const TileCost& tc, int planes) {
+  const int64_t tiles = (int64_t)tc.ntk * tc.ntj;
+  const double Rm = tiled::RAMP_MID_Q / 4.0;
+  double V = 0;
+  for (int64_t t = 0; t < tiles; ++t) V += planes * tc.weight(t) + Rm;
+  std::vector<int64_t> cuts(G + 1);
+  int64_t t = 0;
+  double acc = 0;   // cost of tiles [0, t)
+  for (int64_t b = 0; b < G; ++b) {
+    const double target = V * (double)b / (double)G;
+    while (t < tiles && acc + planes * tc.weight(t) + Rm <= target) {
+      acc += planes * tc.weight(t) + Rm;
+      ++t;
+    }
+    int64_t p = 0;
+    if (t < tiles) {
+      const double off = target - acc - Rm;
+      p = off > 0 ? (int64_t)(off / tc.weight(t) + 0.5) : 0;
+      p = std::min<int64_t>(p, planes);
+    }
+    cuts[b] = std::min<int64_t>(t * planes + p, tiles * planes);
+  }
+  cuts[G] = tiles * planes;
+  for (int64_t b = 1; b <= G; ++b) cuts[b] = std::max(cuts[b], cuts[b - 1]);
+  return cuts;
+}
+
+struct Launch { int64_t ctas; int aligned; const int64_t* cuts; };
+
+Launch pick_launch(int ntk, int ntj, int planes, int wrap, int variant, cudaStream_t s,
+                   bool allow_table = true) {
+  const int64_t tiles = (int64_t)ntk * ntj;
   const int64_t total = tiles * planes;
-  if (g_tiled_ctas > 0) return {std::min<int64_t>(g_tiled_ctas, total), tiled::SPLIT_ALIGNED};
-  static std::map<std::pair<int64_t, int>, Launch> cache;
-  const auto key = std::make_pair(tiles, planes);
+  if (g_tiled_ctas > 0)
+    return {std::min<int64_t>(g_tiled_ctas, total), tiled::SPLIT_ALIGNED, nullptr};
+  const TileCost tc{ntk, ntj, (wrap & 4) != 0, (wrap & 2) != 0, edge_scale(variant)};
+  using Key = std::tuple<int, int, int, int, int>;
+  static std::map<Key, Launch> cache;
+  const Key key{ntk, ntj, planes, (wrap & 6) | (allow_table ? 8 : 0), variant};
   const auto hit = cache.find(key);
   if (hit != cache.end()) return hit->second;
   const int64_t G0 = std::max<int64_t>(1, std::min<int64_t>(num_sms(), total / 4));
-  Launch best{G0, tiled::SPLIT_CONTIGUOUS};
-  double best_cost = split_cost(G0, tiles, planes, tiled::SPLIT_CONTIGUOUS);
-  const double cb = split_cost(G0, tiles, planes, tiled::SPLIT_BALANCED);
-  if (cb < best_cost - 1e-9) { best_cost = cb; best = {G0, tiled::SPLIT_BALANCED}; }
+  Launch best{G0, tiled::SPLIT_CONTIGUOUS, nullptr};
+  double best_cost = split_cost(G0, tc, planes, tiled::SPLIT_CONTIGUOUS);
+  const double cb = split_cost(G0, tc, planes, tiled::SPLIT_BALANCED);
+  if (cb < best_cost - 1e-9) { best_cost = cb; best = {G0, tiled::SPLIT_BALANCED, nullptr}; }
   for (int64_t G = tiles; G <= G0; ++G) {
-    const double c = split_cost(G, tiles, planes, tiled::SPLIT_ALIGNED);
-    if (c < best_cost - 1e-9) { best_cost = c; best = {G, tiled::SPLIT_ALIGNED}; }
+    const double c = split_cost(G, tc, planes, tiled::SPLIT_ALIGNED);
+    if (c < best_cost - 1e-9) { best_cost = c; best = {G, tiled::SPLIT_ALIGNED, nullptr}; }
   }
-  cache[key] = best;
+  // the edge-weighted table needs a device copy of the cuts: made once per
+  // geometry, never while the stream is being captured into a graph
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusNone && allow_table) {
+    const std::vector<int64_t> cuts = table_cuts(G0, tc, planes);
+    const double ct = split_cost(G0, tc, planes, tiled::SPLIT_TABLE, cuts.data());
+    if (ct < best_cost - 1e-9) {
+      int64_t* d = nullptr;
+      if (cudaMalloc(&d, cuts.size() * sizeof(int64_t)) == cudaSuccess &&
+          cudaMemcpy(d, cuts.data(), cuts.size() * sizeof(int64_t), cudaMemcpyHostToDevice) ==
+              cudaSuccess) {
+        best_cost = ct;
+        best = {G0, tiled::SPLIT_TABLE, d};
+      } else {
+        cudaGetLastError();
+        if (d) cudaFree(d);
+      }
+    }
+  }
+  if (cs == cudaStreamCaptureStatusNone || !allow_table)
+    cache[key] = best;   // (not cached while capturing: decided again later)
   return best;
 }
 
@@ -637,10 +727,10 @@ int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, 
   const int ntj = (g.n1 + tiled::TJ - 1) / tiled::TJ;
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
-  const Launch L = pick_launch(ntk * ntj, nplanes);
+  const Launch L = pick_launch(ntk, ntj, nplanes, wrap, V, s);
   launch_pdl(tiled::k_stage_tiled<V, MODE, LAZY>, dim3((unsigned)L.ctas), dim3(tiled::NT), smem, s,
              m, mg, ms, mp, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes,
-             L.aligned, pf);
+             L.aligned, pf, L.cuts);
   return 0;
 }
 
@@ -657,7 +747,7 @@ int launch_sn2(const CUtensorMap& m, const double* saved, double* out, const Coe
   const int ntj = (g.n1 + tiled::TJ - 1) / tiled::TJ;
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
-  const Launch L = pick_launch(ntk * ntj, nplanes);
+  const Launch L = pick_launch(ntk, ntj, nplanes, wrap, FDNS_SN, s, false);
   launch_pdl(sn2::k_stage_sn2<MODE>, dim3((unsigned)L.ctas), dim3(sn2::NT), sn2::SMEM_BYTES, s,
              m, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes, L.aligned);
   return 0;

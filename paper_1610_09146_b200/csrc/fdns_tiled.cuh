@@ -391,7 +391,8 @@ __device__ __forceinline__ void fill_slots(const Coef& k, const SAcc& a, double*
 // (thread 0) streams the planes of all segments back to back through the
 // ring, prefetching across segment boundaries.
 // Partition modes of the (tile, plane) steps of one launch over G CTAs.
-enum SplitMode : int { SPLIT_CONTIGUOUS = 0, SPLIT_ALIGNED = 1, SPLIT_BALANCED = 2 };
+enum SplitMode : int { SPLIT_CONTIGUOUS = 0, SPLIT_ALIGNED = 1, SPLIT_BALANCED = 2,
+                       SPLIT_TABLE = 3 };
 // Ramp of a segment that starts inside a CTA's range (ring refill, five
 // planes converted, queues rebuilt), in quarter plane steps (measured
 // ~3.3 us vs ~3.0 us per step at 64^3).
@@ -413,9 +414,13 @@ struct Segments {
   //  SPLIT_BALANCED: contiguous ranges of equal cost, a tile counting its
   //    planes plus one mid-range ramp (RAMP_MID_Q), so a CTA whose range
   //    contains a tile start gets correspondingly fewer planes.
+  //  SPLIT_TABLE: host-computed cut points `cuts[0..G]` (edge-weighted
+  //    costs, see fdns_b200.cu:table_cuts).
   static __host__ __device__ __forceinline__ Segments partition(int64_t b, int64_t G,
                                                                 int64_t total, int planes,
-                                                                int mode) {
+                                                                int mode,
+                                                                const int64_t* cuts = nullptr) {
+    if (mode == SPLIT_TABLE) return Segments{cuts[b], cuts[b + 1], planes};
     const int64_t tiles = total / planes;
     if (mode == SPLIT_ALIGNED && G >= tiles) {
       const int64_t base = G / tiles, rem = G % tiles;
@@ -454,7 +459,7 @@ __global__ void __launch_bounds__(NT, 1)
                   const double* __restrict__ work,
                   const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
                   int64_t total_steps, int wrap_mask, int i_lo, int nplanes, int split,
-                  int pf_saved) {
+                  int pf_saved, const int64_t* __restrict__ cuts) {
   extern __shared__ __align__(128) double sm[];
   constexpr bool kBuf = (V == FDNS_SN);
   constexpr bool kGB = (V == FDNS_SS || V == FDNS_RS) && MODE != 2;
@@ -464,7 +469,7 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* gbars = bars + NR;      // SS/RS: the two gradient-box barriers
   const int tid = threadIdx.x;
   const int tk = tid % TK, tj = tid / TK;
-  Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes, split);
+  Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes, split, cuts);
   if (S.beg >= S.end) return;
   trace(0);
 
