@@ -448,6 +448,22 @@ def test_c4_256_steps_match_c_oracle(variant):
     assert np.array_equal(host_cons(st), npo.interior(G[:5], 2))
 
 
+@pytest.mark.parametrize("variant", ["BL", "RA", "RS", "SN", "SS"])
+@pytest.mark.parametrize("npts", [(37, 45, 70), (130, 20, 132), (16, 130, 40)])
+def test_ragged_grids_match_c_oracle(variant, npts):
+    """Non-cubic grids whose extents are not multiples of the 32x8 tile
+    (partial edge tiles, odd plane counts, n2 >= 128 with the sector-aligned
+    point-kernel map, a 1-tile-wide row): three RK3 steps of a perturbed TGV
+    state bitwise equal to the C oracle."""
+    F = npo.manufactured(npts, CO)
+    G = F.copy()
+    c_oracle.run(G, CO, 1e-3, 3)
+    g = grid_of(npts)
+    st = state_from_cons(g, npo.interior(F[:5], 2))
+    fd.run(st, fd.RKScheme(dt=1e-3), fd.ResidualEvaluator(g, C, variant), 3)
+    assert np.array_equal(host_cons(st), npo.interior(G[:5], 2))
+
+
 def test_c5_512_cross_variant_bitwise():
     """Config C5 on one GPU (TGV 512^3, dt=4.2e-4, all four variants; BL's
     60 work arrays put it at ~99 GB of HBM): one RK3 step, all variants
