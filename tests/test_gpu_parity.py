@@ -582,6 +582,55 @@ def test_mass_conservation_short_run():
     assert abs(fd.reduce_sum(st.rho) - m0) <= 1e-10 * abs(m0)
 
 
+@pytest.mark.parametrize("variant", ["SS", "SN"])
+def test_tgv_physics_to_t12(variant):
+    """The reference's TGV acceptance criterion 4 (test_acceptance.py:
+    111-137) on the device: 64^3, dt=3.385e-3, to t=12 with diagnostics every
+    25 iterations -- initial KE 0.125 +- 1e-3 and enstrophy 0.375 +- 1e-2,
+    KE non-increasing for t > 4, and a single enstrophy maximum, in
+    [8, 10]."""
+    g = grid_of((64,) * 3)
+    dt = 3.385e-3
+    niter = int(np.ceil(12.0 / dt))
+    st = fd.taylor_green_init(g, C)
+    rho0 = fd.mean_density(st)
+    rep = fd.run(st, fd.RKScheme(dt=dt), fd.ResidualEvaluator(g, C, variant), niter,
+                 cadence=25, collect=fd.make_collector(g, rho0))
+    rec = rep.records
+    assert abs(rec[0].kinetic_energy - 0.125) <= 1e-3
+    assert abs(rec[0].enstrophy - 0.375) <= 1e-2
+    assert all(b.kinetic_energy <= a.kinetic_energy + 1e-12
+               for a, b in zip(rec, rec[1:]) if b.time > 4.0)
+    en = [(r.time, r.enstrophy) for r in rec]
+    peaks = [en[i][0] for i in range(1, len(en) - 1)
+             if en[i][1] > en[i - 1][1] and en[i][1] > en[i + 1][1]]
+    t_max = max(en, key=lambda q: q[1])[0]
+    assert len(peaks) == 1 and 8.0 <= t_max <= 10.0
+
+
+@pytest.mark.parametrize("variant", ["BL", "RA", "RS", "SN", "SS"])
+def test_residual_sums_conservative(variant):
+    """The reference's criterion 3 (test_acceptance.py:88-108) as the
+    reference itself behaves: the mass and momentum residuals of the 64^3 TGV
+    sum to ~0 relative to their absolute sums (<= 1e-11), the energy
+    residual's relative sum is 1.5e-08 -- the reference records that same
+    value and FAILS its own 1e-11 bound (pkg/test_output.txt:212, the skew
+    split of the energy flux does not telescope exactly) -- and 100 steps
+    keep the total mass to 1e-10."""
+    g = grid_of((64,) * 3)
+    st = fd.taylor_green_init(g, C)
+    res = fd.assemble_residual(st, C, variant)
+    rel = []
+    for f in res.fields:
+        scale = float(f.interior.abs().sum()) + 1e-300
+        rel.append(abs(fd.reduce_sum(f)) / scale)
+    assert max(rel[:4]) <= 1e-11
+    assert rel[4] == pytest.approx(1.5e-8, rel=0.05)
+    m0 = fd.reduce_sum(st.rho)
+    fd.run(st, fd.RKScheme(dt=3.385e-3), fd.ResidualEvaluator(g, C, variant), 100)
+    assert abs(fd.reduce_sum(st.rho) - m0) / abs(m0) <= 1e-10
+
+
 def test_timeseries_csv_from_device_run(tmp_path):
     """diagnostics.py:166-190 round trip of device-sampled records."""
     g = grid_of((16,) * 3)
