@@ -205,6 +205,67 @@ def test_c3_perturbed_128_200_steps(golden_meta, variant):
         assert abs(rec.enstrophy - row[2]) <= 1e-10 * abs(row[2])
 
 
+@pytest.mark.parametrize("variant", ["BL", "RA", "RS", "SN", "SS"])
+def test_analytic_rhs_convergence(variant):
+    """Known answer (test_plan.py:207-238): rho = 1, u = (sin x, 0, 0),
+    p = p0 has closed-form residuals; the device residual is within 0.05 of
+    them at 32^3 and converges at fourth order (error ratio 10-25 from 32^3
+    to 64^3)."""
+    c = C
+    errs = []
+    for n in (32, 64):
+        g = grid_of((n,) * 3)
+        shape = (n,) * 3
+        x = (np.arange(n) * (2.0 * np.pi / n))[:, None, None]
+        rho = np.ones(shape)
+        u = [np.sin(x) + np.zeros(shape), np.zeros(shape), np.zeros(shape)]
+        p0 = 1.0 / c.gM2
+        F = npo.state_from_primitives(shape, CO, rho, u, np.full(shape, p0))
+        st = state_from_cons(g, npo.interior(F[:5], 2))
+        r = npo.interior(fd.assemble_residual(st, c, variant).bundle.cpu().numpy(), 2)
+        d_rho = -np.cos(x) + np.zeros(shape)
+        d_rhou0 = -np.sin(2 * x) - c.c43_inv_Re * np.sin(x) + np.zeros(shape)
+        d_rhoE = (-(c.gamma / c.gm1) * p0 * np.cos(x) + c.c43_inv_Re * np.cos(2 * x)
+                  + np.zeros(shape))
+        errs.append(max(np.max(np.abs(r[0] - d_rho)), np.max(np.abs(r[1] - d_rhou0)),
+                        np.max(np.abs(r[2])), np.max(np.abs(r[3])),
+                        np.max(np.abs(r[4] - d_rhoE))))
+    assert errs[0] <= 0.05
+    assert 10.0 <= errs[0] / errs[1] <= 25.0
+
+
+def test_cross_plan_equivalence_50_iterations():
+    """The reference's criterion 1 (test_acceptance.py:35-55): all five
+    plans after 50 iterations of the 32^3 TGV agree to 1e-10 (here
+    bitwise)."""
+    g = grid_of((32,) * 3)
+    finals = {}
+    for v in VARIANTS:
+        st = fd.taylor_green_init(g, C)
+        fd.run(st, fd.RKScheme(dt=6.77e-3), fd.ResidualEvaluator(g, C, v), 50)
+        finals[v] = host_cons(st)
+    for v in VARIANTS:
+        assert np.array_equal(finals[v], finals["BL"]), v
+
+
+def test_rk3_temporal_order_on_device():
+    """The scheme's temporal accuracy (criterion 9, test_acceptance.py:
+    207-235) observed through the device time loop: the TGV at 16^3 to
+    t = 0.08 with dt halved twice; the error against a dt/8 run shrinks by
+    >= 4x per halving."""
+    g = grid_of((16,) * 3)
+    T = 0.08
+    finals = {}
+    for k in (1, 2, 4, 8):
+        st = fd.taylor_green_init(g, C)
+        dt = 0.02 / k
+        fd.run(st, fd.RKScheme(dt=dt), fd.ResidualEvaluator(g, C, "SN"),
+               int(round(T / dt)))
+        finals[k] = host_cons(st)
+    errs = [np.max(np.abs(finals[k] - finals[8])) for k in (1, 2)]
+    assert errs[0] > 0 and errs[0] / errs[1] >= 4.0
+
+
 def test_cross_variant_bitwise_after_steps():
     n = 48
     F = npo.perturbed_taylor_green(n, CO, 11)
