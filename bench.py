@@ -131,13 +131,17 @@ def cpu_cores() -> int:
     return len(os.sched_getaffinity(0))
 
 
-def run_cpu_oracle(n: int, steps: int, warmup: int = 1, min_seconds: float = 0.0):
+def run_cpu_oracle(npts, steps: int, warmup: int = 1, min_seconds: float = 0.0):
     """The C + OpenMP restatement of the reference path (oracle/), timed on
-    the host cores: pt-stage/s.  Runs `steps` iterations, repeated until at
-    least `min_seconds` of CPU work has been timed."""
+    the host cores: pt-stage/s.  `npts` is n (a cube: the TGV) or a grid
+    tuple (a weak-scaled slab grid: the manufactured smooth state of the
+    same shape).  Runs `steps` iterations, repeated until at least
+    `min_seconds` of CPU work has been timed."""
     from oracle import c_oracle, numpy_oracle as npo
     c = npo.Consts()
-    F = npo.taylor_green(n, c)
+    npts = (npts,) * 3 if isinstance(npts, int) else tuple(npts)
+    n = npts[1]
+    F = npo.taylor_green(n, c) if len(set(npts)) == 1 else npo.manufactured(npts, c)
     c_oracle.run(F, c, DT.get(n, 3.385e-3), warmup)
     done, dt = 0, 0.0
     while done == 0 or dt < min_seconds:
@@ -145,7 +149,7 @@ def run_cpu_oracle(n: int, steps: int, warmup: int = 1, min_seconds: float = 0.0
         c_oracle.run(F, c, DT.get(n, 3.385e-3), steps)
         dt += time.perf_counter() - t0
         done += steps
-    return n ** 3 * 3 * done / dt, dt, done
+    return float(np.prod(npts)) * 3 * done / dt, dt, done
 
 
 # ------------------------------------------------------------------ ours
@@ -493,21 +497,27 @@ def main_reference(args):
     if rank != 0:
         return
     n = args.n
+    # the same grid as our arm: weak scaling stacks one n^3 block per rank
+    npts = (n * world, n, n) if world > 1 and args.scaling == "weak" else (n, n, n)
     steps = max(1, min(args.steps, args.cpu_steps))
-    val, sec, steps = run_cpu_oracle(n, steps, warmup=1,
+    val, sec, steps = run_cpu_oracle(npts, steps, warmup=1,
                                      min_seconds=args.cpu_seconds)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
         "n_gpus": world, "steps": steps, "warmup": 1,
         "ms_per_step": sec / steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: analytic Taylor-Green vortex initial state",
-        "config": {"workload": f"TGV {n}^3 fp64, dt={DT.get(n)}, RK3 steps",
-                   "grid": [n, n, n]},
+        "scaling": args.scaling if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: analytic Taylor-Green vortex initial state"
+                if len(set(npts)) == 1 else
+                "synthetic: smooth manufactured state of the slab grid's shape",
+        "config": {"workload": f"TGV {n}^3 fp64, dt={DT.get(n)}, RK3 steps"
+                               + (f", x{world} ranks (weak)" if npts[0] != n else ""),
+                   "grid": list(npts)},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cpu_cores(),
                          "kind": "port",
                          "sample": f"C+OpenMP restatement of the reference "
-                                   f"(SN route), TGV {n}^3, {steps} steps"},
+                                   f"(SN route), grid {npts}, {steps} steps"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
