@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <map>
+#include <mutex>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -675,6 +676,8 @@ Launch pick_launch(int ntk, int ntj, int planes, int wrap, int variant, cudaStre
   const TileCost tc{ntk, ntj, (wrap & 4) != 0, (wrap & 2) != 0, edge_scale(variant)};
   using Key = std::tuple<int, int, int, int, int>;
   static std::map<Key, Launch> cache;
+  static std::mutex mu;   // ctypes releases the GIL: calls may be concurrent
+  std::lock_guard<std::mutex> lock(mu);
   const Key key{ntk, ntj, planes, (wrap & 6) | (allow_table ? 8 : 0), variant};
   const auto hit = cache.find(key);
   if (hit != cache.end()) return hit->second;
@@ -732,12 +735,11 @@ int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, 
   int pf = 0;
   if constexpr (MODE == 1)
     pf = (g_prefetch_saved && saved != in && saved_map(&ms, saved, g)) ? 1 : 0;
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr;
+  std::call_once(attr, [] {
     cudaFuncSetAttribute(tiled::k_stage_tiled<V, MODE, LAZY>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  });
   const int ntk = (g.n2 + tiled::TK - 1) / tiled::TK;
   const int ntj = (g.n1 + tiled::TJ - 1) / tiled::TJ;
   const int nplanes = i_hi - i_lo;
@@ -752,12 +754,11 @@ int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, 
 template <int MODE>
 int launch_sn2(const CUtensorMap& m, const double* saved, double* out, const Coef& k,
                const Geom& g, double coef, int wrap, int i_lo, int i_hi, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr;
+  std::call_once(attr, [] {
     cudaFuncSetAttribute(sn2::k_stage_sn2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          sn2::SMEM_BYTES);
-    attr = true;
-  }
+  });
   const int ntk = (g.n2 + tiled::TK - 1) / tiled::TK;
   const int ntj = (g.n1 + tiled::TJ - 1) / tiled::TJ;
   const int nplanes = i_hi - i_lo;
@@ -775,18 +776,20 @@ int launch_residual(int variant, const double* in, const double* saved, double* 
   if (i_hi <= i_lo) return 0;
   CUtensorMap m;
   if (variant != FDNS_BL && g_kernel_path != 1 && plane_map(&m, in, g)) {
+    int rc = 0;
     switch (variant) {
-      case FDNS_RA: launch_tiled_v<FDNS_RA, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
-      case FDNS_RS: launch_tiled_v<FDNS_RS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
+      case FDNS_RA: rc = launch_tiled_v<FDNS_RA, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
+      case FDNS_RS: rc = launch_tiled_v<FDNS_RS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
       case FDNS_SN:
-        if (g_kernel_path == 3) launch_sn2<MODE>(m, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
+        if (g_kernel_path == 3) rc = launch_sn2<MODE>(m, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
         else if (g_kernel_path == 4)
-          launch_tiled_v<FDNS_SN, MODE, false>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
-        else launch_tiled_v<FDNS_SN, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
+          rc = launch_tiled_v<FDNS_SN, MODE, false>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
+        else rc = launch_tiled_v<FDNS_SN, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
         break;
-      case FDNS_SS: launch_tiled_v<FDNS_SS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
+      case FDNS_SS: rc = launch_tiled_v<FDNS_SS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
       default: return fail("unknown variant");
     }
+    if (rc) return rc;   // e.g. a tensor map that could not be encoded
     count();
     return check_launch("tiled stage kernel");
   }
