@@ -19,9 +19,10 @@ from .mesh import (ConfigurationError, Field, Grid, halo_exchange,
 from .physics import (ConservativeState, PhysicalConstants, Residual,
                       SolverDivergenceError, eval_primitives_fused,
                       eval_primitives_grouped)
-from .plan import (PLAN_NAMES, KernelPlan, ResidualEvaluator,
-                   assemble_residual, build_plan, plan_storage,
-                   workarray_budget)
+from .plan import (PLAN_NAMES, KernelPlan, KernelSchedule, LoopGroup,
+                   RaceViolation, ResidualEvaluator, assemble_residual,
+                   build_plan, lower_plan, plan_storage,
+                   validate_race_freedom, workarray_budget)
 from .timeloop import (RK3_ALPHA, IterationState, RKScheme, RunReport,
                        advance_iteration, rk_substep, run)
 from .diagnostics import (DiagnosticsRecord, conservation_sums,

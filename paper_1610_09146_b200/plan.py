@@ -51,19 +51,70 @@ VELOCITY_GRADIENT_IDS = tuple(f"D(u{i},x{j})" for i in range(3)
                               for j in range(3))
 
 
+STATE_FIELDS = ("rho", "rhou0", "rhou1", "rhou2", "rhoE")
+POINT_FIELDS = STATE_FIELDS + ("u0", "u1", "u2", "p", "T")
+RESIDUAL_FIELDS = ("d_rho", "d_rhou0", "d_rhou1", "d_rhou2", "d_rhoE")
+
+
+@dataclass(frozen=True)
+class LoopGroup:
+    """One device pass (or a halo barrier) with its grid-field footprint
+    (plan.py:40-47).  Here a group is one kernel of the evaluation."""
+
+    name: str
+    kind: str  # "loop" or "halo"
+    writes: frozenset
+    reads: frozenset
+
+
 @dataclass(frozen=True)
 class KernelPlan:
-    """plan.py:51-58 (loop groups are replaced by the device kernel list)."""
+    """plan.py:51-58; `loop_groups` lists the device passes of one residual
+    evaluation (see `_device_groups`)."""
 
     name: str
     store_derivatives: bool
     derivatives_to_store: frozenset
     local_variables: bool
-    primitives: str  # "grouped" or "fused"
+    primitives: str  # "grouped" or "fused" (the reference's form; the
+    #                  device runs the fused pass, bitwise equal)
+    loop_groups: tuple = ()
 
     @property
     def variant_id(self) -> int:
         return _lib.VARIANT_IDS[self.name]
+
+
+def _wa(did: str) -> str:
+    return "wa_" + did
+
+
+def _device_groups(name: str, storage: dict) -> tuple:
+    """The kernels one evaluation runs, with their field footprints:
+    primitives (one fused pass over the conservative fields, physics.py:
+    185-202); BL: the 54 plain/product fills in one kernel (products formed
+    in registers, no scratch array), the ghost frames of the three inner
+    arrays (the reference's inner halo exchange, plan.py:378-379) and the
+    six mixed fills; RS/SS: the nine velocity gradients (+ their ghost
+    frames) in one kernel; then the residual kernel."""
+    fetched = [d for d in derivative_ids() if storage[d] == FETCH]
+    groups = [LoopGroup("primitives:fused", "loop",
+                        frozenset({"u0", "u1", "u2", "p", "T"}),
+                        frozenset(STATE_FIELDS))]
+    if name == "BL":
+        plain = frozenset(_wa(d) for d in fetched if not d.startswith("DD("))
+        inner = frozenset(_wa(f"D(u{q},x{q})") for q in range(3))
+        cross = frozenset(_wa(d) for d in fetched if d.startswith("DD("))
+        groups += [LoopGroup("fill:plain+products", "loop", plain, frozenset(POINT_FIELDS)),
+                   LoopGroup("halo:velocity-divergence-arrays", "halo", inner, inner),
+                   LoopGroup("fill:cross", "loop", cross, inner)]
+    elif fetched:
+        grads = frozenset(_wa(d) for d in fetched)
+        groups += [LoopGroup("fill:velocity-gradients", "loop", grads,
+                             frozenset({"u0", "u1", "u2"}))]
+    groups.append(LoopGroup("residual", "loop", frozenset(RESIDUAL_FIELDS),
+                            frozenset(POINT_FIELDS) | frozenset(_wa(d) for d in fetched)))
+    return tuple(groups)
 
 
 def build_plan(name: str, spec=None) -> KernelPlan:
@@ -81,7 +132,87 @@ def build_plan(name: str, spec=None) -> KernelPlan:
         "SS": (False, velocity, True, "fused"),
     }
     store, to_store, locals_, prims = table[key]
-    return KernelPlan(key, store, to_store, locals_, prims)
+    plan = KernelPlan(key, store, to_store, locals_, prims)
+    return KernelPlan(key, store, to_store, locals_, prims,
+                      _device_groups(key, plan_storage(plan)))
+
+
+@dataclass(frozen=True)
+class RaceViolation:
+    group: str
+    field: str
+
+
+def validate_race_freedom(plan: KernelPlan) -> list:
+    """plan.py:196-213: the (group, field) pairs where a grid pass writes a
+    field it also reads (halo barriers skipped); [] means race-free."""
+    out = []
+    for g in plan.loop_groups:
+        if g.kind != "loop":
+            continue
+        for f in sorted(g.writes & g.reads):
+            out.append(RaceViolation(g.name, f))
+    return out
+
+
+@dataclass
+class KernelSchedule:
+    """plan.py:229-283: a lowered plan."""
+
+    plan: KernelPlan
+    storage: dict
+    loop_groups: tuple
+
+    @property
+    def fetch_ids(self) -> list:
+        return [d for d in derivative_ids() if self.storage[d] == FETCH]
+
+    @property
+    def inner_halo_ids(self) -> list:
+        """Inner derivatives of the mixed terms read from work arrays."""
+        ids = []
+        for d in derivative_ids():
+            if d.startswith("DD("):
+                inner = f"D(u{d[4]},x{d[4]})"
+                if self.storage[inner] == FETCH and inner not in ids:
+                    ids.append(inner)
+        return ids
+
+    def stencil_applications_per_point(self) -> int:
+        return stencil_applications_per_point(self.plan)
+
+    def listing(self) -> str:
+        """Human-readable schedule (plan.py:266-283 layout)."""
+        lines = [f"plan {self.plan.name}",
+                 f"primitives {self.plan.primitives}",
+                 f"work-array budget {workarray_budget(self.plan)}",
+                 f"stencil applications/point {self.stencil_applications_per_point()}",
+                 "", "loop groups:"]
+        for g in self.loop_groups:
+            lines.append(f"  [{g.kind}] {g.name}")
+            lines.append(f"      writes: {', '.join(sorted(g.writes))}")
+            lines.append(f"      reads:  {', '.join(sorted(g.reads))}")
+        lines += ["", "derivative storage:"]
+        for did in sorted(derivative_ids()):
+            lines.append(f"  {did:24s} {self.storage[did]}")
+        lines.append("")
+        return "\n".join(lines)
+
+
+def lower_plan(plan: KernelPlan, spec=None) -> KernelSchedule:
+    """plan.py:290-310: lower a plan, rejecting racy groups and groups that
+    read a field before any earlier group (or the state) produced it."""
+    violations = validate_race_freedom(plan)
+    if violations:
+        raise ValueError(f"plan {plan.name} is not race-free: {violations}")
+    available = set(STATE_FIELDS)
+    for g in plan.loop_groups:
+        missing = g.reads - available
+        if missing:
+            raise ValueError(f"group {g.name} reads {sorted(missing)} before "
+                             "they are produced")
+        available |= g.writes
+    return KernelSchedule(plan, plan_storage(plan), plan.loop_groups)
 
 
 def plan_storage(plan: KernelPlan, spec=None) -> dict:

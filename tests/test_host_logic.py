@@ -194,3 +194,38 @@ def test_bench_tables_formats(tmp_path):
     bt.write_scaling_csv(sc, tmp_path / "scaling.csv")
     assert (tmp_path / "scaling.csv").read_text().splitlines()[0] == \
         "workers,Nx,Ny,Nz,runtime,normalized,ideal"
+
+
+def test_plan_lowering_and_race_validator():
+    """plan.py:196-310 restated for the device schedule: every shipped plan
+    lowers (race-free, dependencies satisfied); the reference's criterion-10
+    counterexample (a fused primitives pass that reads the velocities it
+    writes, test_acceptance.py:238-260) is rejected naming exactly u0-u2;
+    a pass reading a field nobody produced is rejected."""
+    import dataclasses
+    import pytest
+    import paper_1610_09146_b200 as fd
+    for n in fd.PLAN_NAMES:
+        plan = fd.build_plan(n)
+        assert fd.validate_race_freedom(plan) == []
+        sched = fd.lower_plan(plan)
+        assert sched.fetch_ids == [d for d, c in fd.plan_storage(plan).items() if c == "FETCH"]
+        want_inner = [] if n in ("RA", "SN") else ["D(u0,x0)", "D(u1,x1)", "D(u2,x2)"]
+        assert sched.inner_halo_ids == want_inner
+        text = sched.listing()
+        assert f"plan {n}" in text and "loop groups:" in text
+        assert f"stencil applications/point {sched.stencil_applications_per_point()}" in text
+    bad_group = fd.LoopGroup(
+        "primitives:bad-fusion", "loop", frozenset({"u0", "u1", "u2", "p"}),
+        frozenset({"rho", "rhou0", "rhou1", "rhou2", "rhoE", "u0", "u1", "u2"}))
+    template = fd.build_plan("BL")
+    bad = dataclasses.replace(template, loop_groups=(bad_group,) + template.loop_groups[1:])
+    assert {(v.group, v.field) for v in fd.validate_race_freedom(bad)} == {
+        ("primitives:bad-fusion", "u0"), ("primitives:bad-fusion", "u1"),
+        ("primitives:bad-fusion", "u2")}
+    with pytest.raises(ValueError, match="not race-free"):
+        fd.lower_plan(bad)
+    early = fd.LoopGroup("fill:early", "loop", frozenset({"wa_x"}), frozenset({"T"}))
+    unsat = dataclasses.replace(template, loop_groups=(early,) + template.loop_groups)
+    with pytest.raises(ValueError, match="before they are produced"):
+        fd.lower_plan(unsat)
