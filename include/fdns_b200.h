@@ -63,6 +63,14 @@ int32_t fdns_primitives(double* state, const fdns_problem* pb, void* stream);
 int32_t fdns_halo_wrap(double* fields, int32_t nf, int32_t axes_mask,
                        const fdns_problem* pb, void* stream);
 
+/* One 4th-order stencil applied to one padded field `f` (halo current),
+ * written to the interior of `out` (not aliasing f): op 0-2 = first
+ * derivative along that axis, 3-5 = second derivative along axis op-3 --
+ * replaces stencil.first_derivative / second_derivative
+ * (stencil.py:71-102). */
+int32_t fdns_derivative(const double* f, double* out, int32_t op,
+                        const fdns_problem* pb, void* stream);
+
 /* Residual of a state bundle (primitives and halos current) under a variant;
  * writes the interior of the 5 residual fields -- replaces
  * ResidualEvaluator.evaluate (plan.py:394-416) and the generated kernel

@@ -18,7 +18,10 @@ from .mesh import (ConfigurationError, Field, Grid, halo_exchange,
                    live_field_count, make_grid, reduce_sum)
 from .physics import (ConservativeState, PhysicalConstants, Residual,
                       SolverDivergenceError, eval_primitives_fused,
-                      eval_primitives_grouped)
+                      eval_primitives_grouped, heat_flux, skew_convective,
+                      stress_tensor)
+from .stencil import (cross_derivative, first_derivative, grid_weights,
+                      make_weights, second_derivative)
 from .plan import (PLAN_NAMES, KernelPlan, KernelSchedule, LoopGroup,
                    RaceViolation, ResidualEvaluator, assemble_residual,
                    build_plan, lower_plan, plan_storage,
@@ -28,7 +31,7 @@ from .timeloop import (RK3_ALPHA, IterationState, RKScheme, RunReport,
 from .diagnostics import (DiagnosticsRecord, conservation_sums,
                           enstrophy_integral, kinetic_energy_integral,
                           make_collector, mean_density, read_timeseries,
-                          taylor_green_init, write_timeseries)
+                          taylor_green_init, vorticity, write_timeseries)
 from .decomp import Slab
 
 __version__ = "0.1.0"

@@ -343,6 +343,22 @@ __global__ void __launch_bounds__(256) k_grad_ss_all(const double* __restrict__ 
   }
 }
 
+// One stencil applied to one padded field, interior points only
+// (stencil.py:71-102): first derivative along `op` (0-2) or second
+// derivative along `op - 3`.  Same expression shapes as the residual's.
+template <int OP>
+__global__ void __launch_bounds__(256) k_derivative(const double* __restrict__ f,
+                                                    double* __restrict__ out, Coef k, Geom g) {
+  const int kk = point_k(g);
+  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
+  const int ii = blockIdx.z;
+  if (kk < 0 || kk >= g.n2 || jj >= g.n1) return;
+  const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
+  const GAcc a{f, c, g.s0, g.s1, 0};
+  if constexpr (OP < 3) out[c] = d1<OP, E_FIELD, 0, 0>(k, a);
+  else out[c] = d2<OP - 3, 0>(k, a);
+}
+
 // RK update on the interior of 5 fields (timeloop.py:80-85).
 __global__ void k_rk_update(double* cons, const double* saved, const double* __restrict__ res,
                             double coef, Geom g) {
@@ -916,6 +932,28 @@ int32_t fdns_primitives(double* state, const fdns_problem* pb, void* stream) {
   k_primitives<<<blocks, 256, 0, (cudaStream_t)stream>>>(state, k, g.fs);
   count();
   return check_launch("primitives kernel");
+}
+
+int32_t fdns_derivative(const double* f, double* out, int32_t op, const fdns_problem* pb,
+                        void* stream) {
+  if (int e = validate(pb)) return e;
+  if (op < 0 || op > 5) return fail("fdns_derivative: op must be 0-2 (first) or 3-5 (second)");
+  if (f == out) return fail("fdns_derivative: output must not alias the input");
+  const Geom g = make_geom(pb);
+  const Coef k = make_coef(pb);
+  const dim3 blk(32, 8, 1);
+  const dim3 grd = point_grid(g, blk);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (op) {
+    case 0: k_derivative<0><<<grd, blk, 0, s>>>(f, out, k, g); break;
+    case 1: k_derivative<1><<<grd, blk, 0, s>>>(f, out, k, g); break;
+    case 2: k_derivative<2><<<grd, blk, 0, s>>>(f, out, k, g); break;
+    case 3: k_derivative<3><<<grd, blk, 0, s>>>(f, out, k, g); break;
+    case 4: k_derivative<4><<<grd, blk, 0, s>>>(f, out, k, g); break;
+    default: k_derivative<5><<<grd, blk, 0, s>>>(f, out, k, g); break;
+  }
+  count();
+  return check_launch("derivative kernel");
 }
 
 int32_t fdns_halo_wrap(double* fields, int32_t nf, int32_t axes_mask, const fdns_problem* pb,

@@ -179,3 +179,43 @@ def eval_primitives_grouped(state: ConservativeState,
     equal to the fused form (test_physics.py:83-100); on the device both run
     as the one fused pass."""
     return eval_primitives_fused(state, c)
+
+
+# -- building blocks of the unexpanded residual (physics.py:205-253) --------
+def stress_tensor(grad_u, c: PhysicalConstants):
+    """Symmetric viscous stress tau[i][j] = (1/Re)(du_i/dx_j + du_j/dx_i)
+    minus (2/(3Re)) div u on the diagonal, from the nine gradients
+    grad_u[i][j] (scalars, arrays or device tensors); same operation order
+    as physics.py:205-221, so the same bits."""
+    div = grad_u[0][0] + grad_u[1][1] + grad_u[2][2]
+
+    def entry(i, j):
+        sym = c.inv_Re * (grad_u[i][j] + grad_u[j][i])
+        return sym - c.c23_inv_Re * div if i == j else sym
+
+    upper = {(i, j): entry(i, j) for i in range(3) for j in range(i, 3)}
+    return [[upper[min(i, j), max(i, j)] for j in range(3)] for i in range(3)]
+
+
+def heat_flux(grad_T, c: PhysicalConstants):
+    """Fourier heat flux heat_coeff * dT/dx_j per axis (physics.py:224-226)."""
+    return [c.heat_coeff * g for g in grad_T]
+
+
+def skew_convective(phi, uj, rho, axis: int):
+    """Skew-symmetric convective split along one axis (physics.py:229-253):
+    half the sum of d(rho phi u_j), u_j d(rho phi) and rho phi d(u_j) along
+    x_j; phi a Field or the scalar 1.  Products are formed over the padded
+    arrays (device tensors), the derivatives by the device stencil."""
+    from .mesh import Field
+    from .stencil import first_derivative
+    grid = uj.grid
+    m = Field(grid)                       # rho * phi
+    m.data.copy_(rho.data * (phi.data if isinstance(phi, Field) else float(phi)))
+    flux = Field(grid)                    # rho * phi * u_j
+    flux.data.copy_(m.data * uj.data)
+    d_flux, d_m, d_u = (first_derivative(f, axis) for f in (flux, m, uj))
+    out = Field(grid)
+    out.interior[...] = 0.5 * (d_flux.interior + uj.interior * d_m.interior
+                               + m.interior * d_u.interior)
+    return out

@@ -37,6 +37,9 @@ def grid_of(npts):
     return fd.make_grid(npts, (TWO_PI,) * 3)
 
 
+U0_F = 5   # bundle index of u0 (physics.py:115-119)
+
+
 def state_from_cons(grid, cons):
     from paper_1610_09146_b200.diagnostics import state_from_conservative
     return state_from_conservative(grid, C, cons)
@@ -264,6 +267,66 @@ def test_rk3_temporal_order_on_device():
         finals[k] = host_cons(st)
     errs = [np.max(np.abs(finals[k] - finals[8])) for k in (1, 2)]
     assert errs[0] > 0 and errs[0] / errs[1] >= 4.0
+
+
+def test_field_stencil_operators_match_oracle():
+    """stencil.first/second/cross_derivative on device Fields (the reference's
+    field-level operators, stencil.py:71-121) bitwise equal to the oracle's
+    stencils; the interior only is written (halo stays zero)."""
+    npts = (20, 36, 28)
+    F = npo.manufactured(npts, CO)
+    g = grid_of(npts)
+    w = npo.grid_weights(npts)
+    f = fd.Field(g)
+    f.data.copy_(torch.from_numpy(np.ascontiguousarray(F[U0_F])))
+    for axis in range(3):
+        d = fd.first_derivative(f, axis).numpy()
+        assert np.array_equal(npo.interior(d, 2), npo.d1(F[U0_F], 2, axis, w))
+        assert np.all(d[:2] == 0) and np.all(d[:, :, -2:] == 0)
+        d2 = fd.second_derivative(f, axis).numpy()
+        assert np.array_equal(npo.interior(d2, 2), npo.d2(F[U0_F], 2, axis, w))
+    inner = np.zeros_like(F[U0_F])
+    npo.interior(inner, 2)[...] = npo.d1(F[U0_F], 2, 2, w)
+    npo.halo_exchange(inner[None], 2)
+    want = npo.d1(inner, 2, 0, w)
+    assert np.array_equal(npo.interior(fd.cross_derivative(f, 0, 2).numpy(), 2), want)
+    with pytest.raises(ValueError):
+        fd.cross_derivative(f, 1, 1)
+
+
+def test_vorticity_and_physics_helpers():
+    """diagnostics.vorticity, physics.stress_tensor / heat_flux /
+    skew_convective (physics.py:205-253) on the device, bitwise equal to the
+    same formulas over the oracle's stencils."""
+    npts = (16, 20, 24)
+    F = npo.manufactured(npts, CO)
+    g = grid_of(npts)
+    w = npo.grid_weights(npts)
+    st = state_from_cons(g, npo.interior(F[:5], 2))
+    P = st.bundle.cpu().numpy()
+    d = {(q, a): npo.d1(P[U0_F + q], 2, a, w) for q in range(3) for a in range(3)}
+    om = fd.vorticity(st)
+    want = [d[(2, 1)] - d[(1, 2)], d[(0, 2)] - d[(2, 0)], d[(1, 0)] - d[(0, 1)]]
+    for got, ref in zip(om, want):
+        assert np.array_equal(npo.interior(got.numpy(), 2), ref)
+    grad = [[torch.from_numpy(np.ascontiguousarray(d[(q, a)])).cuda() for a in range(3)]
+            for q in range(3)]
+    tau = fd.stress_tensor(grad, C)
+    div = d[(0, 0)] + d[(1, 1)] + d[(2, 2)]
+    for i in range(3):
+        for j in range(3):
+            ref = C.inv_Re * (d[(i, j)] + d[(j, i)])
+            if i == j:
+                ref = ref - C.c23_inv_Re * div
+            assert np.array_equal(tau[i][j].cpu().numpy(), ref)
+    q = fd.heat_flux([grad[0][0]], C)[0]
+    assert np.array_equal(q.cpu().numpy(), C.heat_coeff * d[(0, 0)])
+    sk = fd.skew_convective(st.u[1], st.u[0], st.rho, 0).numpy()
+    m = P[0] * P[U0_F + 1]
+    fl = m * P[U0_F]
+    ref = 0.5 * (npo.d1(fl, 2, 0, w) + npo.interior(P[U0_F], 2) * npo.d1(m, 2, 0, w)
+                 + npo.interior(m, 2) * npo.d1(P[U0_F], 2, 0, w))
+    assert np.array_equal(npo.interior(sk, 2), ref)
 
 
 def test_cross_variant_bitwise_after_steps():
