@@ -33,5 +33,6 @@ from .diagnostics import (DiagnosticsRecord, conservation_sums,
                           make_collector, mean_density, read_timeseries,
                           taylor_green_init, vorticity, write_timeseries)
 from .decomp import Slab
+from . import terms
 
 __version__ = "0.1.0"

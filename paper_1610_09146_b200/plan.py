@@ -215,17 +215,25 @@ def lower_plan(plan: KernelPlan, spec=None) -> KernelSchedule:
     return KernelSchedule(plan, plan_storage(plan), plan.loop_groups)
 
 
-def plan_storage(plan: KernelPlan, spec=None) -> dict:
+def storage_classes(name: str, store_derivatives: bool,
+                    derivatives_to_store: frozenset, local_variables: bool,
+                    spec=None) -> dict:
     """Storage class per derivative id (plan.py:61-73)."""
     out = {}
     for did in derivative_ids():
-        if plan.store_derivatives or did in plan.derivatives_to_store:
+        if store_derivatives or did in derivatives_to_store:
             out[did] = FETCH
-        elif plan.local_variables:
+        elif local_variables:
             out[did] = LOCAL
         else:
             out[did] = INLINE
     return out
+
+
+def plan_storage(plan: KernelPlan, spec=None) -> dict:
+    """Storage class per derivative id of a plan (plan.py:188-193)."""
+    return storage_classes(plan.name, plan.store_derivatives,
+                           plan.derivatives_to_store, plan.local_variables, spec)
 
 
 def stencil_applications_per_point(plan: KernelPlan) -> int:
@@ -407,3 +415,10 @@ def assemble_residual(state: ConservativeState, constants: PhysicalConstants,
     ev = ResidualEvaluator(state.grid, constants, plan, spec, workers)
     out = Residual(state.grid)
     return ev.evaluate(state, out)
+
+
+# The reference's product scratch array name (plan.py:37).  The device fill
+# forms products in registers, so no plan allocates it (workarray_budget).
+SCRATCH = "scratch0"
+
+from .terms import DEFAULT_SPEC  # noqa: E402  (terms reads this module's tables)

@@ -229,3 +229,23 @@ def test_plan_lowering_and_race_validator():
     unsat = dataclasses.replace(template, loop_groups=(early,) + template.loop_groups)
     with pytest.raises(ValueError, match="before they are produced"):
         fd.lower_plan(unsat)
+
+
+def test_terms_registry_matches_reference_goldens(golden_meta):
+    """terms.build_residual_spec (terms.py:135-200): the 60 derivatives (42
+    d1 incl. 18 product targets, 12 d2, 6 cross), their occurrence counts
+    pinned to the reference's own spec, the nine velocity-gradient ids and
+    the reference's identifier spelling; only the internal-energy form."""
+    import pytest
+    import paper_1610_09146_b200 as fd
+    spec = fd.terms.build_residual_spec()
+    kinds = [d.kind for d in spec.derivatives.values()]
+    assert (kinds.count("d1"), kinds.count("d2"), kinds.count("cross")) == (42, 12, 6)
+    assert sum(d.is_product for d in spec.derivatives.values()) == 18
+    assert spec.occurrences == golden_meta["occurrences"]
+    assert len(spec.velocity_gradient_ids) == 9
+    assert spec.derivatives["DD(u1,x0,x1)"].inner_id == "D(u1,x1)"
+    assert spec.derivatives["D(rhou0*u1,x1)"].name == "d_rhou0u1_x1"
+    assert fd.plan.DEFAULT_SPEC.occurrences == spec.occurrences
+    with pytest.raises(ValueError):
+        fd.terms.build_residual_spec("total")
