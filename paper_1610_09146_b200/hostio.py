@@ -24,6 +24,7 @@ launch of host time.  Results are bitwise those of `advance_iteration`.
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -44,25 +45,56 @@ class HostStepper:
     modify it only after `wait()` and a synchronize."""
 
     def __init__(self, state: ConservativeState, evaluator: ResidualEvaluator,
-                 scheme: RKScheme, host: torch.Tensor, chunks: int = 5,
+                 scheme: RKScheme, host, chunks: int = 5,
                  graphs: bool | None = None, upload: str = "ce"):
-        if not host.is_pinned() or host.dtype != torch.float64 or \
-                tuple(host.shape) != (5,) + tuple(state.bundle.shape[1:]):
-            raise ValueError("host must be a pinned float64 (5, padded...) "
-                             "tensor (HostStepper.pinned_buffers)")
+        """`host`: a pinned float64 (5, padded...) tensor
+        (`pinned_buffers`), or the reference's own five padded numpy arrays
+        (rho, rhou0, rhou1, rhou2, rhoE as `Field.data` holds them), which
+        are page-locked in place (cudaHostRegister) until `close()`."""
+        shape = tuple(state.bundle.shape[1:])
+        self._registered = []
+        if isinstance(host, torch.Tensor):
+            if not host.is_pinned() or host.dtype != torch.float64 or \
+                    tuple(host.shape) != (5,) + shape:
+                raise ValueError("host must be a pinned float64 (5, padded...) "
+                                 "tensor (HostStepper.pinned_buffers)")
+            fields = [host[f] for f in range(5)]
+        else:
+            arrays = list(host)
+            if len(arrays) != 5 or any(
+                    not isinstance(a, np.ndarray) or a.dtype != np.float64 or
+                    a.shape != shape or not a.flags.c_contiguous for a in arrays):
+                raise ValueError("host must be five C-contiguous float64 padded "
+                                 f"arrays of shape {shape}")
+            cudart = torch.cuda.cudart()
+            for a in arrays:
+                err = cudart.cudaHostRegister(a.ctypes.data, a.nbytes, 0)
+                if int(err) != 0:
+                    self.close()
+                    raise _lib.FdnsError(f"cudaHostRegister failed ({int(err)})")
+                self._registered.append(a)
+            fields = [torch.from_numpy(a) for a in arrays]
         self.state = state
         self.ev = evaluator
         self.scheme = scheme
         self.host = host
+        self._host_fields = fields
         self.it = IterationState(state, saved=False)
         self.h2d = torch.cuda.Stream()
         self.d2h = torch.cuda.Stream()
-        # the five conservative fields are one contiguous block on both
-        # sides; it is copied as `chunks` contiguous pieces
-        d, h = state.bundle[:5].reshape(-1), host.reshape(-1)
-        n = d.numel()
-        cuts = [(n * c // chunks) & ~1 for c in range(chunks)] + [n]  # 16-byte cuts
-        self._pairs = [(d[a:b], h[a:b]) for a, b in zip(cuts, cuts[1:]) if b > a]
+        # copied as `chunks` contiguous pieces: of the five-field block when
+        # the host side is one block too, else of each field
+        if isinstance(host, torch.Tensor):
+            sides = [(state.bundle[:5].reshape(-1), host.reshape(-1), chunks)]
+        else:
+            per = max(1, chunks // 5)
+            sides = [(state.bundle[f].reshape(-1), fields[f].reshape(-1), per)
+                     for f in range(5)]
+        self._pairs = []
+        for d, h, k in sides:
+            n = d.numel()
+            cuts = [(n * c // k) & ~1 for c in range(k)] + [n]   # 16-byte cuts
+            self._pairs += [(d[a:b], h[a:b]) for a, b in zip(cuts, cuts[1:]) if b > a]
         self._lib = _lib.load()
         if upload not in ("sm", "ce"):
             raise ValueError("upload must be 'sm' or 'ce'")
@@ -126,7 +158,7 @@ class HostStepper:
         # warm every program once eagerly on a side stream (first-use setup
         # of the library and allocator), on a scratch copy of the state
         saved = self.state.bundle.clone()
-        host_saved = self.host.clone()
+        host_saved = [h.clone() for h in self._host_fields]
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
@@ -142,7 +174,8 @@ class HostStepper:
             graphs[which] = g
         torch.cuda.synchronize()
         self.state.bundle.copy_(saved)
-        self.host.copy_(host_saved)
+        for h, hs in zip(self._host_fields, host_saved):
+            h.copy_(hs)
         torch.cuda.synchronize()
         self._graphs = graphs
 
@@ -155,6 +188,16 @@ class HostStepper:
         self._pending = True
         self.it.time += self.scheme.dt
         self.it.iteration += 1
+
+    def close(self) -> None:
+        """Release the page-locking of registered numpy arrays (after the
+        last `wait()` and a synchronize)."""
+        if self._registered:
+            torch.cuda.synchronize()
+            cudart = torch.cuda.cudart()
+            for a in self._registered:
+                cudart.cudaHostUnregister(a.ctypes.data)
+            self._registered = []
 
     def wait(self) -> None:
         """Download the last step's result into the host buffer; the buffer

@@ -797,6 +797,27 @@ def test_host_stepper_matches_run(variant, graphs, chunks):
     assert stepper.it.iteration == 5
 
 
+def test_host_stepper_on_reference_numpy_arrays():
+    """HostStepper over five plain padded numpy arrays (the reference's own
+    Field.data layout), page-locked in place: the arrays end up holding the
+    run() result bitwise."""
+    from paper_1610_09146_b200.hostio import HostStepper
+    g = grid_of((24, 20, 16))
+    F = npo.manufactured((24, 20, 16), CO)
+    ref = state_from_cons(g, npo.interior(F[:5], 2))
+    fd.run(ref, fd.RKScheme(dt=2e-3), fd.ResidualEvaluator(g, C, "SN"), 3)
+    st = state_from_cons(g, npo.interior(F[:5], 2))
+    arrays = [np.ascontiguousarray(a) for a in st.bundle[:5].cpu().numpy()]
+    stepper = HostStepper(st, fd.ResidualEvaluator(g, C, "SN"), fd.RKScheme(dt=2e-3),
+                          arrays, chunks=10)
+    for _ in range(3):
+        stepper.step()
+    stepper.wait()
+    torch.cuda.synchronize()
+    stepper.close()
+    assert np.array_equal(np.stack(arrays), ref.bundle[:5].cpu().numpy())
+
+
 def test_host_stepper_sees_host_edits():
     """A modification of the host buffer between wait() and the next step()
     is what the next step advances (the upload is real)."""
