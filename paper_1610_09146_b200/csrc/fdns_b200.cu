@@ -359,6 +359,29 @@ __global__ void __launch_bounds__(256) k_derivative(const double* __restrict__ f
   else out[c] = d2<OP - 3, 0>(k, a);
 }
 
+// SS/RS interior fill as a 3-D grid of 32x8 point blocks (plane per
+// blockIdx.z, sector-aligned columns): the nine velocity gradients
+// ws[q*3+a] = D(u_q, x_a); the diagonal ghost frames follow in k_diag_ghost.
+__global__ void __launch_bounds__(256) k_grad_ss_interior(const double* __restrict__ in,
+                                                          double* __restrict__ ws, Coef k,
+                                                          Geom g) {
+  const int kk = point_k(g);
+  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
+  const int ii = blockIdx.z;
+  if (kk < 0 || kk >= g.n2 || jj >= g.n1) return;
+  const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
+  const GAcc a{in, c, g.s0, g.s1, g.fs};
+  ws[(0 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U0, 0>(k, a);
+  ws[(0 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U0, 0>(k, a);
+  ws[(0 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U0, 0>(k, a);
+  ws[(1 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U1, 0>(k, a);
+  ws[(1 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U1, 0>(k, a);
+  ws[(1 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U1, 0>(k, a);
+  ws[(2 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U2, 0>(k, a);
+  ws[(2 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U2, 0>(k, a);
+  ws[(2 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U2, 0>(k, a);
+}
+
 // RK update on the interior of 5 fields (timeloop.py:80-85).
 __global__ void k_rk_update(double* cons, const double* saved, const double* __restrict__ res,
                             double coef, Geom g) {
@@ -824,6 +847,9 @@ int launch_residual(int variant, const double* in, const double* saved, double* 
   return check_launch("residual kernel");
 }
 
+// A/B switch: FDNS_SS_FILL_1D=1 selects the one-launch grid-stride SS fill.
+const bool g_ss_fill_3d = std::getenv("FDNS_SS_FILL_1D") == nullptr;
+
 // Work-array fills that precede the residual kernel (BL, RS, SS).
 int launch_fills(int variant, const double* in, double* work, const Coef& k, const Geom& g,
                  cudaStream_t s) {
@@ -846,6 +872,15 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
     k_fill_cross<<<grd, blk, 0, s>>>(work, k, g);
     count(3);
     return check_launch("BL fills");
+  }
+  // SS/RS fill: from n2 >= 128 on the 3-D point-block kernel + the ghost
+  // frames (+6% SS/RS steps at 256^3); below, one grid-stride launch
+  // (its single launch wins at 64^3: -4% otherwise)
+  if ((variant == FDNS_SS || variant == FDNS_RS) && g_ss_fill_3d && g.n2 >= 128) {
+    k_grad_ss_interior<<<grd, blk, 0, s>>>(in, work, k, g);
+    ghosts(work + 0 * g.fs, work + 4 * g.fs, work + 8 * g.fs);
+    count(2);
+    return check_launch("SS fills");
   }
   if (variant == FDNS_SS || variant == FDNS_RS) {
     {   // 9 gradients on the interior + the diagonal ghost frames, one launch
