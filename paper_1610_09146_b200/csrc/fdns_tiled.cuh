@@ -452,6 +452,10 @@ struct Segments {
   }
 };
 
+#ifndef FDNS_EARLY_GV
+#define FDNS_EARLY_GV 1
+#endif
+
 template <int V, int MODE, bool LAZY = true>
 __global__ void __launch_bounds__(NT, 1)
     k_stage_tiled(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tgw,
@@ -567,6 +571,42 @@ __global__ void __launch_bounds__(NT, 1)
           while (issued < total_pos && issued < w + NR) issue_next();
         }
       }
+      const int i = i_seg + t;
+      // this step's global loads are issued first, so their latency runs
+      // under the plane's arrival conversion and the barrier: the saved
+      // state (MODE 1) and, for SS/RS, the stored gradients (the axis-0
+      // queue heads and the six off-diagonal values at the point);
+      // inactive (edge) threads read a valid clamped column, never written
+      const int64_t cl = (int64_t)(i + g.h) * g.s0 + (int64_t)(min(jj, g.n1 - 1) + g.h) * g.s1 +
+                         (min(kk, g.n2 - 1) + g.h);
+      double sv[5];
+      if constexpr (MODE == 1) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) sv[f] = saved[f * g.fs + cl];
+      }
+      double gv[9];
+      if constexpr (kGB && FDNS_EARLY_GV) {
+        const double* w11 = work + 4 * g.fs + cl;   // stored D(u1,x1)
+        const double* w22 = work + 8 * g.fs + cl;   // stored D(u2,x2)
+        if (t == 0) {
+#pragma unroll
+          for (int d = 0; d < 5; ++d) {
+            q1[d] = __ldg(w11 + (d - 2) * g.s0);
+            q2[d] = __ldg(w22 + (d - 2) * g.s0);
+          }
+        } else {
+#pragma unroll
+          for (int d = 0; d < 4; ++d) { q1[d] = q1[d + 1]; q2[d] = q2[d + 1]; }
+          q1[4] = __ldg(w11 + 2 * g.s0);
+          q2[4] = __ldg(w22 + 2 * g.s0);
+        }
+        gv[0 * 3 + 1] = __ldg(work + 1 * g.fs + cl);
+        gv[0 * 3 + 2] = __ldg(work + 2 * g.fs + cl);
+        gv[1 * 3 + 0] = __ldg(work + 3 * g.fs + cl);
+        gv[1 * 3 + 2] = __ldg(work + 5 * g.fs + cl);
+        gv[2 * 3 + 0] = __ldg(work + 6 * g.fs + cl);
+        gv[2 * 3 + 1] = __ldg(work + 7 * g.fs + cl);
+      }
       if (t == 0) {
         for (int d = 0; d < 5; ++d) {
           const int pp = w + d;
@@ -650,7 +690,6 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
 
-      const int i = i_seg + t;
       if constexpr (MODE == 2) {   // BL fill: derivative arrays only
         if (active) {
           const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(jj + g.h) * g.s1 + (kk + g.h);
@@ -664,14 +703,6 @@ __global__ void __launch_bounds__(NT, 1)
       double r[NFIELDS];
 #pragma unroll
       for (int f = 0; f < NFIELDS; ++f) r[f] = a.v(f, 0, 0, 0);   // r[RHOE_F] = rho*e
-      // issue the saved-state loads now; they land while the residual runs
-      double sv[5];
-      if constexpr (MODE == 1) {
-        const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(min(jj, g.n1 - 1) + g.h) * g.s1 +
-                          (min(kk, g.n2 - 1) + g.h);
-#pragma unroll
-        for (int f = 0; f < 5; ++f) sv[f] = saved[f * g.fs + c];
-      }
       double R[5];
       if constexpr (V == FDNS_SN) {
         if constexpr (LAZY) {
@@ -687,30 +718,28 @@ __global__ void __launch_bounds__(NT, 1)
         InlineProvider<SAcc> P(k, a);
         residual_point<true>(k, P, r, R);
       } else {  // SS / RS: stored velocity gradients from the work arrays
-        // inactive (edge) threads read a valid clamped column; never written
-        const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(min(jj, g.n1 - 1) + g.h) * g.s1 +
-                          (min(kk, g.n2 - 1) + g.h);
-        const double* w11 = work + 4 * g.fs + c;   // stored D(u1,x1)
-        const double* w22 = work + 8 * g.fs + c;   // stored D(u2,x2)
-        if (t == 0) {
+        if constexpr (!FDNS_EARLY_GV) {
+          const double* w11 = work + 4 * g.fs + cl;   // stored D(u1,x1)
+          const double* w22 = work + 8 * g.fs + cl;   // stored D(u2,x2)
+          if (t == 0) {
 #pragma unroll
-          for (int d = 0; d < 5; ++d) {
-            q1[d] = __ldg(w11 + (d - 2) * g.s0);
-            q2[d] = __ldg(w22 + (d - 2) * g.s0);
+            for (int d = 0; d < 5; ++d) {
+              q1[d] = __ldg(w11 + (d - 2) * g.s0);
+              q2[d] = __ldg(w22 + (d - 2) * g.s0);
+            }
+          } else {
+#pragma unroll
+            for (int d = 0; d < 4; ++d) { q1[d] = q1[d + 1]; q2[d] = q2[d + 1]; }
+            q1[4] = __ldg(w11 + 2 * g.s0);
+            q2[4] = __ldg(w22 + 2 * g.s0);
           }
-        } else {
-#pragma unroll
-          for (int d = 0; d < 4; ++d) { q1[d] = q1[d + 1]; q2[d] = q2[d + 1]; }
-          q1[4] = __ldg(w11 + 2 * g.s0);
-          q2[4] = __ldg(w22 + 2 * g.s0);
+          gv[0 * 3 + 1] = __ldg(work + 1 * g.fs + cl);
+          gv[0 * 3 + 2] = __ldg(work + 2 * g.fs + cl);
+          gv[1 * 3 + 0] = __ldg(work + 3 * g.fs + cl);
+          gv[1 * 3 + 2] = __ldg(work + 5 * g.fs + cl);
+          gv[2 * 3 + 0] = __ldg(work + 6 * g.fs + cl);
+          gv[2 * 3 + 1] = __ldg(work + 7 * g.fs + cl);
         }
-        double gv[9];
-        gv[0 * 3 + 1] = __ldg(work + 1 * g.fs + c);
-        gv[0 * 3 + 2] = __ldg(work + 2 * g.fs + c);
-        gv[1 * 3 + 0] = __ldg(work + 3 * g.fs + c);
-        gv[1 * 3 + 2] = __ldg(work + 5 * g.fs + c);
-        gv[2 * 3 + 0] = __ldg(work + 6 * g.fs + c);
-        gv[2 * 3 + 1] = __ldg(work + 7 * g.fs + c);
         mbar_wait(&gbars[gs & 1], (gs >> 1) & 1);
         const double* gb = bufs0 + (gs & 1) * NGB * PLANE + toff;
         const TiledSSProvider<V == FDNS_RS> P{k, a, q1, q2, gb, gb + PLANE, gb + 2 * PLANE, gv};
