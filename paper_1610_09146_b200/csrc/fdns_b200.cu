@@ -19,6 +19,7 @@
 #include "fdns_math.cuh"
 #include "fdns_tiled.cuh"
 #include "fdns_sn2.cuh"
+#include "fdns_tiled12.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -555,7 +556,7 @@ bool grad_prefetch_map(CUtensorMap* m, const double* work, const Geom& g) {
   return r == CUDA_SUCCESS;
 }
 
-bool plane_map(CUtensorMap* m, const double* base, const Geom& g) {
+bool plane_map(CUtensorMap* m, const double* base, const Geom& g, int box_j = tiled::PJ) {
   const int64_t P2 = g.n2 + 2 * g.h, P1 = g.n1 + 2 * g.h, P0 = g.n0 + 2 * g.h;
   // 16-byte rows, and an even innermost box start (k0 + h - 2): an odd one
   // (odd h) is only 8-byte aligned and the bulk tensor copy faults on it
@@ -566,7 +567,7 @@ bool plane_map(CUtensorMap* m, const double* base, const Geom& g) {
   cuuint64_t dims[4] = {(cuuint64_t)P2, (cuuint64_t)P1, (cuuint64_t)P0, (cuuint64_t)NFIELDS};
   cuuint64_t strides[3] = {(cuuint64_t)(P2 * 8), (cuuint64_t)(P1 * P2 * 8),
                            (cuuint64_t)(g.fs * 8)};
-  cuuint32_t box[4] = {tiled::PK, tiled::PJ, 1, tiled::NLOAD};
+  cuuint32_t box[4] = {tiled::PK, (cuuint32_t)box_j, 1, tiled::NLOAD};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -576,7 +577,7 @@ bool plane_map(CUtensorMap* m, const double* base, const Geom& g) {
 
 // Saved-state tile of one plane (TK x TJ x 1 x 5 conservative fields), the
 // box the stage kernel's L2 prefetch requests.
-bool saved_map(CUtensorMap* m, const double* saved, const Geom& g) {
+bool saved_map(CUtensorMap* m, const double* saved, const Geom& g, int box_j = tiled::TJ) {
   const int64_t P2 = g.n2 + 2 * g.h, P1 = g.n1 + 2 * g.h, P0 = g.n0 + 2 * g.h;
   if (P2 % 2 != 0 || g.h % 2 != 0) return false;
   if (reinterpret_cast<uintptr_t>(saved) % 16 != 0) return false;
@@ -585,7 +586,7 @@ bool saved_map(CUtensorMap* m, const double* saved, const Geom& g) {
   cuuint64_t dims[4] = {(cuuint64_t)P2, (cuuint64_t)P1, (cuuint64_t)P0, 5};
   cuuint64_t strides[3] = {(cuuint64_t)(P2 * 8), (cuuint64_t)(P1 * P2 * 8),
                            (cuuint64_t)(g.fs * 8)};
-  cuuint32_t box[4] = {tiled::TK, tiled::TJ, 1, 5};
+  cuuint32_t box[4] = {tiled::TK, (cuuint32_t)box_j, 1, 5};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(saved), dims,
                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -790,6 +791,32 @@ int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, 
   return 0;
 }
 
+// The 12-warp SN stage kernel (fdns_tiled12.cuh): its own 36 x 16 plane box.
+template <int MODE>
+int launch_t12(const double* in, const double* saved, double* out, const Coef& k, const Geom& g,
+               double coef, int wrap, int i_lo, int i_hi, cudaStream_t s) {
+  CUtensorMap m, ms;
+  if (!plane_map(&m, in, g, t12::PJ)) return fail("plane tensor map");
+  ms = m;
+  int pf = 0;
+  if constexpr (MODE == 1)
+    pf = (g_prefetch_saved && saved != in && saved_map(&ms, saved, g, t12::TJ)) ? 1 : 0;
+  static std::once_flag attr;
+  std::call_once(attr, [] {
+    cudaFuncSetAttribute(t12::k_stage_t12<FDNS_SN, MODE>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, t12::SMEM_BYTES);
+  });
+  const int ntk = (g.n2 + t12::TK - 1) / t12::TK;
+  const int ntj = (g.n1 + t12::TJ - 1) / t12::TJ;
+  const int nplanes = i_hi - i_lo;
+  const int64_t total = (int64_t)ntk * ntj * nplanes;
+  const Launch L = pick_launch(ntk, ntj, nplanes, wrap, FDNS_SN | 0x100, s);
+  launch_pdl(t12::k_stage_t12<FDNS_SN, MODE>, dim3((unsigned)L.ctas), dim3(t12::NT),
+             t12::SMEM_BYTES, s, m, ms, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes,
+             L.aligned, pf, L.cuts);
+  return 0;
+}
+
 template <int MODE>
 int launch_sn2(const CUtensorMap& m, const double* saved, double* out, const Coef& k,
                const Geom& g, double coef, int wrap, int i_lo, int i_hi, cudaStream_t s) {
@@ -821,6 +848,7 @@ int launch_residual(int variant, const double* in, const double* saved, double* 
       case FDNS_RS: rc = launch_tiled_v<FDNS_RS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
       case FDNS_SN:
         if (g_kernel_path == 3) rc = launch_sn2<MODE>(m, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
+        else if (g_kernel_path == 5) rc = launch_t12<MODE>(in, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
         else if (g_kernel_path == 4)
           rc = launch_tiled_v<FDNS_SN, MODE, false>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
         else rc = launch_tiled_v<FDNS_SN, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);

@@ -297,14 +297,15 @@ struct TiledLocalProvider {
 // Lazily evaluated SN provider over the staged tile: a derivative is
 // evaluated where it is used (repeated uses merged by the compiler), the
 // diagonal velocity gradients and mixed terms come from the buffers/queues.
-struct TiledLazyProvider {
+template <class A, int B2P>
+struct TiledLazyProviderT {
   const Coef& k;
-  const SAcc& a;
+  const A& a;
   const double* q1;   // D(u1,x1) at this column, planes i-2..i+2
   const double* q2;   // D(u2,x2)
   const double* b0;   // D(u0,x0) centre of the box buffer (pitch PK)
   const double* b1;   // D(u1,x1) centre (pitch PK)
-  const double* b2;   // D(u2,x2) centre (pitch PK)
+  const double* b2;   // D(u2,x2) centre (pitch B2P)
   template <int A_, int L, int OCC = 0>
   __device__ __forceinline__ double g() const {
     if constexpr (L == S_U + A_) {
@@ -324,12 +325,13 @@ struct TiledLazyProvider {
       constexpr int s = O == 1 ? PK : 1;
       return k.w1[O] * (b0[s] - b0[-s]) + k.w2[O] * (b0[2 * s] - b0[-2 * s]);
     } else if constexpr (J == 2) {
-      return k.w1[1] * (b2[PK] - b2[-PK]) + k.w2[1] * (b2[2 * PK] - b2[-2 * PK]);
+      return k.w1[1] * (b2[B2P] - b2[-B2P]) + k.w2[1] * (b2[2 * B2P] - b2[-2 * B2P]);
     } else {
       return k.w1[2] * (b1[1] - b1[-1]) + k.w2[2] * (b1[2] - b1[-2]);
     }
   }
 };
+using TiledLazyProvider = TiledLazyProviderT<SAcc, PK>;
 
 // SS / RS provider over the staged tile with FETCHed gradients staged too:
 // the centre plane's stored D(u0,x0), D(u1,x1), D(u2,x2) are a TMA box in

@@ -1,0 +1,297 @@
+// fdns_tiled12.cuh -- the 12-warp SN stage kernel.
+//
+// Same z-marching, TMA-fed scheme as fdns_tiled.cuh (read that first), laid
+// out so that 12 warps fit on an SM instead of 8.  The 8-warp kernel is
+// latency bound: its FP64 pipe is ~44% busy, and ncu's dominant stall is the
+// fixed-latency dependency wait of the bitwise-fixed expression chains, which
+// only more resident warps can hide.  What limits the warps is shared memory
+// (a 6-slot ring of ten 36 x 12 field planes is 203 KB), so this kernel:
+//
+//  * uses a 32 x 12 column tile (384 threads, <= 168 registers each): the
+//    staged box 36 x 16 carries 1.5x the tile's points instead of 1.69x;
+//  * stores nine fields per plane slot, not ten: p is not staged but formed
+//    at each tap as gm1 * (rho*e), the expression the arrival conversion
+//    stored before (physics.py:195-202), so the bits are unchanged;
+//  * runs a 5-slot ring (the stencil window itself) with no spare prefetch
+//    slot: each step reads its column's nine values on the oldest plane
+//    (axis-0 offset -2) into registers before the step barrier, after which
+//    that slot is free and the producer streams the next plane into it, a
+//    whole step ahead of its use;
+//  * keeps the centre-plane buffers compact: D(u1,x1) over the tile's rows
+//    only, D(u2,x2) over its columns only (pitch TK).
+//
+// 5 x 41.5 KB ring + 2 x 11.9 KB buffers = 231.7 KB of the 227 KB-per-CTA
+// limit (232448 B).
+#pragma once
+
+#include "fdns_tiled.cuh"
+
+namespace fdns {
+namespace t12 {
+
+using tiled::mbar_expect_tx;
+using tiled::mbar_init;
+using tiled::mbar_wait;
+using tiled::Segments;
+using tiled::tma_load_plane;
+using tiled::tma_prefetch_l2;
+
+constexpr int TK = 32, TJ = 12, NT = TK * TJ;
+constexpr int PK = TK + 4, PJ = TJ + 4;
+constexpr int PLANE = PK * PJ;
+constexpr int NSF = 9;                  // staged fields: rho, rhou0..2, rho*e, u0..2, T
+constexpr int SF_T = 8;                 // slot index of T
+constexpr int SLOT = NSF * PLANE;
+constexpr int NLOAD = 8;                // TMA-loaded fields (rho..u2)
+constexpr uint32_t LOAD_BYTES = NLOAD * PLANE * 8;
+constexpr int NR = 5;                   // ring depth = the stencil window
+constexpr int BU1_N = TJ * PK;          // D(u1,x1): tile rows, all box columns
+constexpr int BU2_N = PJ * TK;          // D(u2,x2): all box rows, tile columns (pitch TK)
+constexpr int BUFSET = PLANE + BU1_N + BU2_N;
+constexpr int SMEM_BYTES = NR * SLOT * 8 + 2 * BUFSET * 8 + 64;
+static_assert(SMEM_BYTES <= 232448, "12-warp tile exceeds the 227 KB shared-memory limit");
+static_assert(PLANE <= 2 * NT && BU1_N <= 2 * NT && BU2_N <= 2 * NT,
+              "per-plane items: at most two per thread");
+
+__device__ __forceinline__ constexpr int sfield(int f) { return f == TF ? SF_T : f; }
+
+// Accessor of the staged window.  Taps at axis-0 offset -2 come from the
+// registers m2 (read before the step barrier: that slot is being refilled by
+// then); the SN provider only taps the oldest plane at its own column.
+struct SAcc12 {
+  static constexpr bool kInternalEnergy = true;
+  static constexpr bool kMaskTaps = true;
+  const double* p[5];   // p[0] unused (the -2 plane is in m2)
+  double m2[NSF];
+  double gm1;
+  __device__ __forceinline__ double raw(int f, int di, int dj, int dk) const {
+    const int sf = sfield(f);
+    if (di == -2) return m2[sf];
+    return p[di + 2][sf * PLANE + dj * PK + dk];
+  }
+  __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
+    if (f == PF) return gm1 * raw(RHOE_F, di, dj, dk);   // p = gm1 * rho*e
+    return raw(f, di, dj, dk);
+  }
+};
+
+// Accessor over all five window planes in shared memory (the centre-plane
+// buffers, before the step barrier).
+struct SAccW {
+  static constexpr bool kInternalEnergy = true;
+  static constexpr bool kMaskTaps = true;
+  const double* p[5];
+  __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
+    return p[di + 2][sfield(f) * PLANE + dj * PK + dk];
+  }
+};
+
+// Arrival conversion (fdns_tiled.cuh:stage_arrival without the p field).
+__device__ __forceinline__ void stage_arrival(const Coef& k, double* slot, int tid) {
+#pragma unroll 1
+  for (int x = tid; x < PLANE; x += NT) {
+    const double rho = slot[RHO * PLANE + x];
+    const double e = slot[RHOE_F * PLANE + x] -
+                     0.5 * (slot[RU0 * PLANE + x] * slot[U0 * PLANE + x] +
+                            slot[RU1 * PLANE + x] * slot[U1 * PLANE + x] +
+                            slot[RU2 * PLANE + x] * slot[U2 * PLANE + x]);
+    const double p = k.gm1 * e;
+    slot[RHOE_F * PLANE + x] = e;
+    slot[SF_T * PLANE + x] = k.gM2 * p / rho;
+  }
+}
+
+template <int V, int MODE>
+__global__ void __launch_bounds__(NT, 1)
+    k_stage_t12(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tsv,
+                const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
+                int64_t total_steps, int wrap_mask, int i_lo, int nplanes, int split,
+                int pf_saved, const int64_t* __restrict__ cuts) {
+  static_assert(V == FDNS_SN, "12-warp kernel: SN");
+  extern __shared__ __align__(128) double sm[];
+  double* bufs0 = sm + NR * SLOT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NR * SLOT + 2 * BUFSET);
+  const int tid = threadIdx.x;
+  const int tk = tid % TK, tj = tid / TK;
+  Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes, split, cuts);
+  if (S.beg >= S.end) return;
+  tiled::trace(0);
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NR; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  tiled::trace(1);
+
+  // producer cursor (thread 0), as in k_stage_tiled
+  int64_t p_seg = S.beg;
+  int p_r = 0, issued = 0;
+  int p_len = 0, p_c0 = 0, p_c1 = 0, p_plane = 0, p_slot = 0;
+  auto enter_segment = [&]() {
+    const int64_t tile = p_seg / nplanes;
+    p_len = (int)(S.seg_end(p_seg) - p_seg) + 4;
+    p_c0 = (int)(tile % ntk) * TK + g.h - 2;
+    p_c1 = (int)(tile / ntk) * TJ + g.h - 2;
+    p_plane = i_lo + (int)(p_seg % nplanes) - 2 + g.h;
+  };
+  if (tid == 0) enter_segment();
+  auto issue_next = [&]() {
+    mbar_expect_tx(&bars[p_slot], LOAD_BYTES);
+    tma_load_plane(sm + p_slot * SLOT, &tin, &bars[p_slot], p_c0, p_c1, p_plane + p_r);
+    if (MODE == 1 && pf_saved && p_r >= 2 && p_r < p_len - 2)
+      tma_prefetch_l2(&tsv, p_c0 + 2, p_c1 + 2, p_plane + p_r);
+    ++issued;
+    p_slot = p_slot + 1 == NR ? 0 : p_slot + 1;
+    if (++p_r == p_len) {
+      p_r = 0;
+      p_seg = S.seg_end(p_seg);
+      if (p_seg < S.end) enter_segment();
+    }
+  };
+  int total_pos = 0;
+  for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) total_pos += (int)(S.seg_end(x) - x) + 4;
+  if (tid == 0)
+    while (issued < total_pos && issued < NR) issue_next();
+
+  int w = 0, wsl = 0;
+  auto slot_of = [&](int d) {
+    const int x = wsl + d;
+    return x >= NR ? x - NR : x;
+  };
+  for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) {
+    const int64_t se = S.seg_end(x);
+    const int64_t tile = x / nplanes;
+    const int k0 = (int)(tile % ntk) * TK, j0 = (int)(tile / ntk) * TJ;
+    const int jj = j0 + tj, kk = k0 + tk;
+    const bool active = jj < g.n1 && kk < g.n2;
+    const int toff = (tj + 2) * PK + (tk + 2);
+    const int nsteps = (int)(se - x);
+    const int i_seg = i_lo + (int)(x % nplanes);
+    double q1[5], q2[5];
+    for (int t = 0; t < nsteps; ++t, ++w, wsl = (wsl + 1 == NR ? 0 : wsl + 1)) {
+      if (t == 0 && w > 0) {
+        // segment change: the new window's five planes; the ring slots of
+        // the previous segment are free once every thread is past it
+        __syncthreads();
+        if (tid == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          while (issued < total_pos && issued < w + NR) issue_next();
+        }
+      }
+      const int i = i_seg + t;
+      const int64_t cl = (int64_t)(i + g.h) * g.s0 + (int64_t)(min(jj, g.n1 - 1) + g.h) * g.s1 +
+                         (min(kk, g.n2 - 1) + g.h);
+      double sv[5];
+      if constexpr (MODE == 1) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) sv[f] = saved[f * g.fs + cl];
+      }
+      if (t == 0) {
+        for (int d = 0; d < 5; ++d) {
+          mbar_wait(&bars[slot_of(d)], ((w + d) / NR) & 1);
+          stage_arrival(k, sm + slot_of(d) * SLOT, tid);
+        }
+      } else {
+        mbar_wait(&bars[slot_of(4)], ((w + 4) / NR) & 1);
+        stage_arrival(k, sm + slot_of(4) * SLOT, tid);
+      }
+      double* bufs = bufs0 + (w & 1) * BUFSET;
+      double* bu1 = bufs + PLANE - 2 * PK;   // row 2 of the box at offset PLANE
+      double* bu2 = bufs + PLANE + BU1_N;    // (row, column - 2), pitch TK
+      {
+        const double* base[5];
+#pragma unroll
+        for (int d = 0; d < 5; ++d) base[d] = sm + slot_of(d) * SLOT;
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const int x0 = tid + m * NT;   // D(u0,x0), whole box
+          if (x0 < PLANE) {
+            SAccW b;
+#pragma unroll
+            for (int d = 0; d < 5; ++d) b.p[d] = base[d] + x0;
+            bufs[x0] = d1<0, E_FIELD, U0, 0>(k, b);
+          }
+          const int y1 = tid + m * NT;   // D(u1,x1), rows 2..TJ+1
+          if (y1 < BU1_N) {
+            const int pos = 2 * PK + y1;
+            SAccW b;
+            b.p[2] = base[2] + pos;
+            bu1[pos] = d1<1, E_FIELD, U1, 0>(k, b);
+          }
+          const int y2 = tid + m * NT;   // D(u2,x2), cols 2..TK+1
+          if (y2 < BU2_N) {
+            const int row = y2 / TK, col = y2 % TK;
+            SAccW b;
+            b.p[2] = base[2] + row * PK + 2 + col;
+            bu2[y2] = d1<2, E_FIELD, U2, 0>(k, b);
+          }
+        }
+      }
+      // axis-0 queues of D(u1,x1), D(u2,x2) at this column (before the
+      // barrier: at a segment start they read the oldest slot too)
+      if (t == 0) {
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+          SAccW b;
+          b.p[2] = sm + slot_of(d) * SLOT + toff;
+          q1[d] = d1<1, E_FIELD, U1, 0>(k, b);
+          q2[d] = d1<2, E_FIELD, U2, 0>(k, b);
+        }
+      } else {
+#pragma unroll
+        for (int d = 0; d < 4; ++d) { q1[d] = q1[d + 1]; q2[d] = q2[d + 1]; }
+        SAccW b;
+        b.p[2] = sm + slot_of(4) * SLOT + toff;
+        q1[4] = d1<1, E_FIELD, U1, 0>(k, b);
+        q2[4] = d1<2, E_FIELD, U2, 0>(k, b);
+      }
+
+      // this column's values on the oldest plane, before its slot is reused
+      SAcc12 a;
+      a.gm1 = k.gm1;
+      {
+        const double* old = sm + slot_of(0) * SLOT + toff;
+#pragma unroll
+        for (int f = 0; f < NSF; ++f) a.m2[f] = old[f * PLANE];
+      }
+      __syncthreads();
+      if (w == 0) tiled::trace(2);
+      if (tid == 0 && issued < total_pos && issued < w + NR + 1) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_next();   // the next plane, into the oldest slot
+      }
+#pragma unroll
+      for (int d = 0; d < 5; ++d) a.p[d] = sm + slot_of(d) * SLOT + toff;
+      a.p[0] = nullptr;
+
+      double r[NFIELDS];
+#pragma unroll
+      for (int f = 0; f < NFIELDS; ++f) r[f] = a.v(f, 0, 0, 0);   // r[RHOE_F] = rho*e
+      double R[5];
+      {
+        const tiled::TiledLazyProviderT<SAcc12, TK> P{
+            k, a, q1, q2, bufs + toff, bu1 + toff, bu2 + (tj + 2) * TK + tk};
+        residual_point<true>(k, P, r, R);
+      }
+      if (active) {
+        if constexpr (MODE == 0) {
+          tiled::emit<5>(out, g, i, jj, kk, R, 0);
+        } else {
+          double q[NFIELDS];
+          tiled::stage_update(sv, R, coef, q);
+          tiled::emit<tiled::NOUT_STAGE>(out, g, i, jj, kk, q, wrap_mask);
+        }
+      }
+    }
+    w += 4;
+    wsl = w % NR;
+  }
+  tiled::trace(3);
+}
+
+}  // namespace t12
+}  // namespace fdns

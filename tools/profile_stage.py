@@ -19,8 +19,11 @@ def main():
     ap.add_argument("--n", type=int, default=128)
     ap.add_argument("--variants", default="SN")
     ap.add_argument("--stages", type=int, default=2)
+    ap.add_argument("--path", type=int, default=0, help="fdns_set_kernel_path (A/B)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
+    from paper_1610_09146_b200 import _lib
+    _lib.load().fdns_set_kernel_path(a.path)
     g = fd.make_grid((a.n,) * 3, (2 * np.pi,) * 3)
     c = fd.PhysicalConstants()
     for v in a.variants.split(","):

@@ -25,9 +25,11 @@ def main():
     ap.add_argument("--sizes", default="64,128,256")
     ap.add_argument("--variants", default="SN,RA,SS")
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--path", type=int, default=0, help="fdns_set_kernel_path (A/B)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     lib = _lib.load()
+    lib.fdns_set_kernel_path(a.path)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     c = fd.PhysicalConstants()
     out = {}
