@@ -108,10 +108,12 @@ int32_t fdns_stage_planes(int32_t variant, const double* in,
                           const fdns_problem* pb, void* stream);
 
 /* Test hook selecting the kernel family: 0 = default (TMA-staged tiled
- * kernels where the row pitch allows), 1 = one-thread-per-point kernels
- * (global-memory taps) for every variant, 3 = default but SN on two warp
- * groups per point (experimental; slower on B200).  All
- * paths are parity-tested. */
+ * kernels where the row pitch allows; SN on the 12-warp kernel where its
+ * tile rows fit the grid), 1 = one-thread-per-point kernels (global-memory
+ * taps) for every variant; SN only: 2 = the 8-warp tiled kernel, 3 = two
+ * warp groups per point (experimental; slower on B200),
+ * 4 = eagerly evaluated derivatives, 5 = the 12-warp kernel.  All paths are
+ * parity-tested. */
 void fdns_set_kernel_path(int32_t path);
 
 /* Test hook: force the persistent tiled kernels onto `ctas` CTAs (0 =

@@ -29,7 +29,8 @@ using namespace fdns;
 namespace {
 
 thread_local std::string g_err;
-int g_kernel_path = 0;        // test hook: 0 default, 1 point kernels, 3 two-group SN
+int g_kernel_path = 0;        // test hook: 0 default, 1 point kernels, 2 8-warp SN, 3 two-group SN,
+                              // 4 eager-local SN, 5 12-warp SN
 int g_tiled_ctas = 0;         // test hook: force the tiled grid size (0 = one per SM)
 std::atomic<long long> g_launches{0};
 inline void count(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
@@ -791,6 +792,14 @@ int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, 
   return 0;
 }
 
+// SN kernel choice: the 12-warp kernel where its 12-row tiles waste few rows
+// (measured whole RK3 steps: +8% at 256^3, +5.5% at 128^3; at 64^3, where
+// the last tile row holds 4 of 12 rows, -6%, so the 8-warp kernel stays).
+inline bool use_t12(const Geom& g) {
+  const int rows = (g.n1 + t12::TJ - 1) / t12::TJ * t12::TJ;
+  return g.n1 >= 96 && 20 * (rows - g.n1) <= g.n1;
+}
+
 // The 12-warp SN stage kernel (fdns_tiled12.cuh): its own 36 x 16 plane box.
 template <int MODE>
 int launch_t12(const double* in, const double* saved, double* out, const Coef& k, const Geom& g,
@@ -848,7 +857,8 @@ int launch_residual(int variant, const double* in, const double* saved, double* 
       case FDNS_RS: rc = launch_tiled_v<FDNS_RS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
       case FDNS_SN:
         if (g_kernel_path == 3) rc = launch_sn2<MODE>(m, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
-        else if (g_kernel_path == 5) rc = launch_t12<MODE>(in, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
+        else if (g_kernel_path == 5 || (g_kernel_path == 0 && use_t12(g)))
+          rc = launch_t12<MODE>(in, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
         else if (g_kernel_path == 4)
           rc = launch_tiled_v<FDNS_SN, MODE, false>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
         else rc = launch_tiled_v<FDNS_SN, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);

@@ -427,14 +427,14 @@ def test_tiled_segment_transitions(kernel_path, variant, ctas):
 def test_sn_kernel_families_agree(kernel_path, ctas):
     """SN on one warp group with lazily evaluated derivatives (default), with
     the eager local array (path 4), on two warp groups (path 3), on the
-    12-warp kernel (path 5) and on the point kernels (path 1): bitwise equal
-    after two RK3 steps."""
+    8-warp (path 2) and 12-warp (path 5) tiled kernels and on the point
+    kernels (path 1): bitwise equal after two RK3 steps."""
     npts = (19, 24, 40)
     F = npo.manufactured(npts, CO)
     g = grid_of(npts)
     cons = npo.interior(F[:5], 2)
     finals = []
-    for path in (1, 3, 4, 5, 0):
+    for path in (1, 2, 3, 4, 5, 0):
         kernel_path.fdns_set_kernel_path(path)
         kernel_path.fdns_set_tiled_grid(ctas)
         st = state_from_cons(g, cons)
