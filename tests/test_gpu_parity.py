@@ -401,10 +401,12 @@ def kernel_path():
 
 @pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("ctas", [3, 7, 13])
-def test_tiled_segment_transitions(kernel_path, variant, ctas):
+@pytest.mark.parametrize("path", [0, 5])
+def test_tiled_segment_transitions(kernel_path, variant, ctas, path):
     """Force the persistent tiled kernel onto few CTAs so each walks several
     (tile, plane-range) segments; results stay bitwise equal to the
-    one-thread-per-point path."""
+    one-thread-per-point path.  Path 5 runs SN/SS/RS on the 12-warp kernel
+    (at this size the default picks the 8-warp one)."""
     npts = (21, 20, 34)
     F = npo.state_from_primitives(npts, CO, np.ones(npts) + 0.01 * np.arange(
         np.prod(npts)).reshape(npts) / np.prod(npts),
@@ -416,7 +418,7 @@ def test_tiled_segment_transitions(kernel_path, variant, ctas):
     a = state_from_cons(g, cons)
     fd.run(a, fd.RKScheme(dt=1e-3), fd.ResidualEvaluator(g, C, variant), 2)
     want = host_cons(a)
-    kernel_path.fdns_set_kernel_path(0)
+    kernel_path.fdns_set_kernel_path(path)
     kernel_path.fdns_set_tiled_grid(ctas)
     b = state_from_cons(g, cons)
     fd.run(b, fd.RKScheme(dt=1e-3), fd.ResidualEvaluator(g, C, variant), 2)
