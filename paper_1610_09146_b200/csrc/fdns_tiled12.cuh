@@ -263,24 +263,30 @@ __global__ void __launch_bounds__(NT, 1)
         const double* base[5];
 #pragma unroll
         for (int d = 0; d < 5; ++d) base[d] = sm + slot_of(d) * SLOT;
+        // items past the first NT of each buffer go to the threads that
+        // converted only one point of the new plane (tid >= PLANE - NT), so
+        // no warp carries much more than the average (max 9 vs 12 units,
+        // a conversion with its division ~3 units)
+        static_assert(PLANE - NT == 192 && BU1_N - NT == 48 && BU2_N - NT == 128,
+                      "item split below assumes the 32 x 12 tile");
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
-          const int x0 = tid + m * NT;   // D(u0,x0), whole box
-          if (x0 < PLANE) {
+          const int x0 = m == 0 ? tid : tid + 192;   // D(u0,x0), whole box
+          if (m == 0 || (tid >= 192 && x0 < PLANE)) {
             SAccW b;
 #pragma unroll
             for (int d = 0; d < 5; ++d) b.p[d] = base[d] + x0;
             bufs[x0] = d1<0, E_FIELD, U0, 0>(k, b);
           }
-          const int y1 = tid + m * NT;   // D(u1,x1), rows 2..TJ+1
-          if (y1 < BU1_N) {
+          const int y1 = m == 0 ? tid : tid + 192;   // D(u1,x1), rows 2..TJ+1
+          if (m == 0 || (tid >= 192 && y1 < BU1_N)) {
             const int pos = 2 * PK + y1;
             SAccW b;
             b.p[2] = base[2] + pos;
             bu1[pos] = d1<1, E_FIELD, U1, 0>(k, b);
           }
-          const int y2 = tid + m * NT;   // D(u2,x2), cols 2..TK+1
-          if (y2 < BU2_N) {
+          const int y2 = m == 0 ? tid : tid + 144;   // D(u2,x2), cols 2..TK+1
+          if (m == 0 || (tid >= 240 && y2 < BU2_N)) {
             const int row = y2 / TK, col = y2 % TK;
             SAccW b;
             b.p[2] = base[2] + row * PK + 2 + col;
