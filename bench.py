@@ -444,7 +444,11 @@ def main_ours(args):
                 "peak": hbm_peak, "unit": "GB/s",
                 "peak_source": f"{hbm_src} (MEASURED_PEAKS.json hbm_gbs)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = measured_traffic(head, n)
+    # contract: `traffic` = dram read+write bytes per launch (a number, or
+    # null); where it comes from goes beside it
+    tr = measured_traffic(head, n)
+    roof["traffic"] = tr["bytes_per_launch"] if tr else None
+    roof["traffic_detail"] = tr
     roof["kernel"] = f"fused stage ({head}): residual+RK update+primitives"
     roof["duration"] = ("average stage launch duration over the timed "
                         "region = timed steps / (3 x steps); L2 flushed "
