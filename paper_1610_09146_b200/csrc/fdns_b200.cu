@@ -540,7 +540,7 @@ bool grad_map(CUtensorMap* m, const double* work, const Geom& g) {
 
 // The nine stored gradients of one plane's tile columns (TK x TJ x 1 x 9),
 // the box the SS/RS stage kernel prefetches into L2.
-bool grad_prefetch_map(CUtensorMap* m, const double* work, const Geom& g, int box_j = tiled::TJ) {
+bool grad_prefetch_map(CUtensorMap* m, const double* work, const Geom& g) {
   const int64_t P2 = g.n2 + 2 * g.h, P1 = g.n1 + 2 * g.h, P0 = g.n0 + 2 * g.h;
   if (P2 % 2 != 0 || g.h % 2 != 0) return false;
   if (reinterpret_cast<uintptr_t>(work) % 16 != 0) return false;
@@ -549,28 +549,9 @@ bool grad_prefetch_map(CUtensorMap* m, const double* work, const Geom& g, int bo
   cuuint64_t dims[4] = {(cuuint64_t)P2, (cuuint64_t)P1, (cuuint64_t)P0, 9};
   cuuint64_t strides[3] = {(cuuint64_t)(P2 * 8), (cuuint64_t)(P1 * P2 * 8),
                            (cuuint64_t)(g.fs * 8)};
-  cuuint32_t box[4] = {tiled::TK, (cuuint32_t)box_j, 1, 9};
+  cuuint32_t box[4] = {tiled::TK, tiled::TJ, 1, 9};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(work), dims,
-                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
-// One field of a bundle (4-D, one field) with a box_k x box_j x 1 box: the
-// 12-warp SS/RS kernel's staged gradient boxes.
-bool field_map(CUtensorMap* m, const double* field, const Geom& g, int box_k, int box_j) {
-  const int64_t P2 = g.n2 + 2 * g.h, P1 = g.n1 + 2 * g.h, P0 = g.n0 + 2 * g.h;
-  if (P2 % 2 != 0 || g.h % 2 != 0) return false;
-  if (reinterpret_cast<uintptr_t>(field) % 16 != 0) return false;
-  auto fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[4] = {(cuuint64_t)P2, (cuuint64_t)P1, (cuuint64_t)P0, 1};
-  cuuint64_t strides[3] = {(cuuint64_t)(P2 * 8), (cuuint64_t)(P1 * P2 * 8),
-                           (cuuint64_t)(P0 * P1 * P2 * 8)};
-  cuuint32_t box[4] = {(cuuint32_t)box_k, (cuuint32_t)box_j, 1, 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(field), dims,
                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -819,38 +800,29 @@ inline bool use_t12(const Geom& g) {
   return g.n1 >= 96 && 20 * (rows - g.n1) <= g.n1;
 }
 
-// The 12-warp stage kernel (fdns_tiled12.cuh): its own 36 x 16 plane box
-// and, for SS/RS, the three compact gradient boxes.
-template <int V, int MODE>
-int launch_t12(const double* in, const double* saved, double* out, const double* work,
-               const Coef& k, const Geom& g, double coef, int wrap, int i_lo, int i_hi,
-               cudaStream_t s) {
-  constexpr bool gb = V == FDNS_SS || V == FDNS_RS;
-  CUtensorMap m, ms, g0, g1, g2, gp;
+// The 12-warp SN stage kernel (fdns_tiled12.cuh): its own 36 x 16 plane box.
+template <int MODE>
+int launch_t12(const double* in, const double* saved, double* out, const Coef& k, const Geom& g,
+               double coef, int wrap, int i_lo, int i_hi, cudaStream_t s) {
+  CUtensorMap m, ms;
   if (!plane_map(&m, in, g, t12::PJ)) return fail("plane tensor map");
-  ms = g0 = g1 = g2 = gp = m;
-  if constexpr (gb)
-    if (!field_map(&g0, work + 0 * g.fs, g, t12::PK, t12::PJ) ||
-        !field_map(&g1, work + 4 * g.fs, g, t12::PK, t12::TJ) ||
-        !field_map(&g2, work + 8 * g.fs, g, t12::TK, t12::PJ) ||
-        !grad_prefetch_map(&gp, work, g, t12::TJ))
-      return fail("gradient tensor map");
+  ms = m;
   int pf = 0;
   if constexpr (MODE == 1)
     pf = (g_prefetch_saved && saved != in && saved_map(&ms, saved, g, t12::TJ)) ? 1 : 0;
   static std::once_flag attr;
   std::call_once(attr, [] {
-    cudaFuncSetAttribute(t12::k_stage_t12<V, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         t12::SMEM_BYTES);
+    cudaFuncSetAttribute(t12::k_stage_t12<FDNS_SN, MODE>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, t12::SMEM_BYTES);
   });
   const int ntk = (g.n2 + t12::TK - 1) / t12::TK;
   const int ntj = (g.n1 + t12::TJ - 1) / t12::TJ;
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
-  const Launch L = pick_launch(ntk, ntj, nplanes, wrap, V | 0x100, s);
-  launch_pdl(t12::k_stage_t12<V, MODE>, dim3((unsigned)L.ctas), dim3(t12::NT), t12::SMEM_BYTES,
-             s, m, ms, g0, g1, g2, gp, work, saved, out, k, g, coef, ntk, total, wrap, i_lo,
-             nplanes, L.aligned, pf, L.cuts);
+  const Launch L = pick_launch(ntk, ntj, nplanes, wrap, FDNS_SN | 0x100, s);
+  launch_pdl(t12::k_stage_t12<FDNS_SN, MODE>, dim3((unsigned)L.ctas), dim3(t12::NT),
+             t12::SMEM_BYTES, s, m, ms, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes,
+             L.aligned, pf, L.cuts);
   return 0;
 }
 
@@ -882,24 +854,16 @@ int launch_residual(int variant, const double* in, const double* saved, double* 
     int rc = 0;
     switch (variant) {
       case FDNS_RA: rc = launch_tiled_v<FDNS_RA, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
-      case FDNS_RS:   // (12-warp kernel only on request: 5-12% slower for SS/RS)
-        if (g_kernel_path == 5)
-          rc = launch_t12<FDNS_RS, MODE>(in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
-        else rc = launch_tiled_v<FDNS_RS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
-        break;
+      case FDNS_RS: rc = launch_tiled_v<FDNS_RS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
       case FDNS_SN:
         if (g_kernel_path == 3) rc = launch_sn2<MODE>(m, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
         else if (g_kernel_path == 5 || (g_kernel_path == 0 && use_t12(g)))
-          rc = launch_t12<FDNS_SN, MODE>(in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
+          rc = launch_t12<MODE>(in, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
         else if (g_kernel_path == 4)
           rc = launch_tiled_v<FDNS_SN, MODE, false>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
         else rc = launch_tiled_v<FDNS_SN, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
         break;
-      case FDNS_SS:   // (12-warp kernel only on request: 5-12% slower for SS/RS)
-        if (g_kernel_path == 5)
-          rc = launch_t12<FDNS_SS, MODE>(in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
-        else rc = launch_tiled_v<FDNS_SS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
-        break;
+      case FDNS_SS: rc = launch_tiled_v<FDNS_SS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
       default: return fail("unknown variant");
     }
     if (rc) return rc;   // e.g. a tensor map that could not be encoded

@@ -340,15 +340,15 @@ using TiledLazyProvider = TiledLazyProviderT<SAcc, PK>;
 // gradients at the point are loaded at step start.  Every value is read from
 // the work arrays (FETCH, plan.py:176-179); mixed terms apply the outer
 // stencil to the stored inner values exactly as codegen.py:111-113 does.
-template <bool INLINE_REST, class A = SAcc, int B2P = PK>
+template <bool INLINE_REST>
 struct TiledSSProvider {
   const Coef& k;
-  const A& a;
+  const SAcc& a;
   const double* q1;   // stored D(u1,x1) at this column, planes i-2..i+2
   const double* q2;   // stored D(u2,x2)
   const double* gb0;  // stored D(u0,x0), centre of the box (pitch PK)
   const double* gb1;  // stored D(u1,x1)
-  const double* gb2;  // stored D(u2,x2) (row pitch B2P)
+  const double* gb2;  // stored D(u2,x2)
   const double* gv;   // off-diagonal D(u_q,x_a) at the point, [q*3+a]
   template <int A_, int L, int OCC = 0>
   __device__ __forceinline__ double g() const {
@@ -371,7 +371,7 @@ struct TiledSSProvider {
       constexpr int s = O == 1 ? PK : 1;
       return k.w1[O] * (gb0[s] - gb0[-s]) + k.w2[O] * (gb0[2 * s] - gb0[-2 * s]);
     } else if constexpr (J == 2) {
-      return k.w1[1] * (gb2[B2P] - gb2[-B2P]) + k.w2[1] * (gb2[2 * B2P] - gb2[-2 * B2P]);
+      return k.w1[1] * (gb2[PK] - gb2[-PK]) + k.w2[1] * (gb2[2 * PK] - gb2[-2 * PK]);
     } else {
       return k.w1[2] * (gb1[1] - gb1[-1]) + k.w2[2] * (gb1[2] - gb1[-2]);
     }

@@ -1,4 +1,4 @@
-// fdns_tiled12.cuh -- the 12-warp stage kernel (SN, SS, RS).
+// fdns_tiled12.cuh -- the 12-warp SN stage kernel.
 //
 // Same z-marching, TMA-fed scheme as fdns_tiled.cuh (read that first), laid
 // out so that 12 warps fit on an SM instead of 8.  The 8-warp kernel is
@@ -101,28 +101,16 @@ __device__ __forceinline__ void stage_arrival(const Coef& k, double* slot, int t
   }
 }
 
-// SS / RS: the three stored diagonal gradients of the centre plane in the
-// same compact layout as SN's buffers -- D(u0,x0) over the box, D(u1,x1)
-// over the tile rows, D(u2,x2) over the tile columns (pitch TK) -- as three
-// TMA boxes (tg0/tg1/tg2), double-buffered by step on gbars.
-constexpr uint32_t GB_BYTES = BUFSET * 8;
-
 template <int V, int MODE>
 __global__ void __launch_bounds__(NT, 1)
     k_stage_t12(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tsv,
-                const __grid_constant__ CUtensorMap tg0, const __grid_constant__ CUtensorMap tg1,
-                const __grid_constant__ CUtensorMap tg2, const __grid_constant__ CUtensorMap tgp,
-                const double* __restrict__ work,
                 const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
                 int64_t total_steps, int wrap_mask, int i_lo, int nplanes, int split,
                 int pf_saved, const int64_t* __restrict__ cuts) {
-  static_assert(V == FDNS_SN || V == FDNS_SS || V == FDNS_RS, "12-warp kernel: SN, SS, RS");
-  constexpr bool kBuf = V == FDNS_SN;
-  constexpr bool kGB = V == FDNS_SS || V == FDNS_RS;
+  static_assert(V == FDNS_SN, "12-warp kernel: SN");
   extern __shared__ __align__(128) double sm[];
-  double* bufs0 = sm + NR * SLOT;   // SN: centre-plane buffers; SS/RS: staged gradients
+  double* bufs0 = sm + NR * SLOT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NR * SLOT + 2 * BUFSET);
-  uint64_t* gbars = bars + NR;
   const int tid = threadIdx.x;
   const int tk = tid % TK, tj = tid / TK;
   Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes, split, cuts);
@@ -132,30 +120,12 @@ __global__ void __launch_bounds__(NT, 1)
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < NR; ++s) mbar_init(&bars[s], 1);
-    if constexpr (kGB) { mbar_init(&gbars[0], 1); mbar_init(&gbars[1], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   tiled::trace(1);
-
-  // SS/RS: the staged gradients of the centre plane of step `gs`
-  auto issue_gb_tile = [&](int gs, int k0, int j0, int plane) {
-    double* dst = bufs0 + (gs & 1) * BUFSET;
-    uint64_t* bar = &gbars[gs & 1];
-    mbar_expect_tx(bar, GB_BYTES);
-    tma_load_plane(dst, &tg0, bar, k0 + g.h - 2, j0 + g.h - 2, plane + g.h);
-    tma_load_plane(dst + PLANE, &tg1, bar, k0 + g.h - 2, j0 + g.h, plane + g.h);
-    tma_load_plane(dst + PLANE + BU1_N, &tg2, bar, k0 + g.h, j0 + g.h - 2, plane + g.h);
-  };
-  auto issue_gb = [&](int gs, int64_t tile, int plane) {
-    issue_gb_tile(gs, (int)(tile % ntk) * TK, (int)(tile / ntk) * TJ, plane);
-  };
-  if constexpr (kGB) {
-    if (tid == 0) issue_gb(0, S.beg / nplanes, i_lo + (int)(S.beg % nplanes));
-  }
-  int gs = 0;   // step counter of this CTA (gradient-box parity)
 
   // producer cursor (thread 0), as in k_stage_tiled
   int64_t p_seg = S.beg;
@@ -174,8 +144,6 @@ __global__ void __launch_bounds__(NT, 1)
     tma_load_plane(sm + p_slot * SLOT, &tin, &bars[p_slot], p_c0, p_c1, p_plane + p_r);
     if (MODE == 1 && pf_saved && p_r >= 2 && p_r < p_len - 2)
       tma_prefetch_l2(&tsv, p_c0 + 2, p_c1 + 2, p_plane + p_r);
-    // SS/RS: the nine stored gradients of this plane's tile columns
-    if constexpr (kGB) tma_prefetch_l2(&tgp, p_c0 + 2, p_c1 + 2, p_plane + p_r);
     ++issued;
     p_slot = p_slot + 1 == NR ? 0 : p_slot + 1;
     if (++p_r == p_len) {
@@ -204,7 +172,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int nsteps = (int)(se - x);
     const int i_seg = i_lo + (int)(x % nplanes);
     double q1[5], q2[5];
-    for (int t = 0; t < nsteps; ++t, ++w, ++gs, wsl = (wsl + 1 == NR ? 0 : wsl + 1)) {
+    for (int t = 0; t < nsteps; ++t, ++w, wsl = (wsl + 1 == NR ? 0 : wsl + 1)) {
       if (t == 0 && w > 0) {
         // segment change: the new window's five planes; the ring slots of
         // the previous segment are free once every thread is past it
@@ -222,31 +190,6 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int f = 0; f < 5; ++f) sv[f] = saved[f * g.fs + cl];
       }
-      // SS/RS: the stored gradients this step reads from global memory (the
-      // axis-0 queue heads, the six off-diagonal values), issued early
-      double gv[9];
-      if constexpr (kGB) {
-        const double* w11 = work + 4 * g.fs + cl;   // stored D(u1,x1)
-        const double* w22 = work + 8 * g.fs + cl;   // stored D(u2,x2)
-        if (t == 0) {
-#pragma unroll
-          for (int d = 0; d < 5; ++d) {
-            q1[d] = __ldg(w11 + (d - 2) * g.s0);
-            q2[d] = __ldg(w22 + (d - 2) * g.s0);
-          }
-        } else {
-#pragma unroll
-          for (int d = 0; d < 4; ++d) { q1[d] = q1[d + 1]; q2[d] = q2[d + 1]; }
-          q1[4] = __ldg(w11 + 2 * g.s0);
-          q2[4] = __ldg(w22 + 2 * g.s0);
-        }
-        gv[0 * 3 + 1] = __ldg(work + 1 * g.fs + cl);
-        gv[0 * 3 + 2] = __ldg(work + 2 * g.fs + cl);
-        gv[1 * 3 + 0] = __ldg(work + 3 * g.fs + cl);
-        gv[1 * 3 + 2] = __ldg(work + 5 * g.fs + cl);
-        gv[2 * 3 + 0] = __ldg(work + 6 * g.fs + cl);
-        gv[2 * 3 + 1] = __ldg(work + 7 * g.fs + cl);
-      }
       if (t == 0) {
         for (int d = 0; d < 5; ++d) {
           mbar_wait(&bars[slot_of(d)], ((w + d) / NR) & 1);
@@ -256,10 +199,10 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_wait(&bars[slot_of(4)], ((w + 4) / NR) & 1);
         stage_arrival(k, sm + slot_of(4) * SLOT, tid);
       }
-      double* bufs = bufs0 + (kGB ? (gs & 1) : (w & 1)) * BUFSET;
+      double* bufs = bufs0 + (w & 1) * BUFSET;
       double* bu1 = bufs + PLANE - 2 * PK;   // row 2 of the box at offset PLANE
       double* bu2 = bufs + PLANE + BU1_N;    // (row, column - 2), pitch TK
-      if constexpr (kBuf) {
+      {
         const double* base[5];
 #pragma unroll
         for (int d = 0; d < 5; ++d) base[d] = sm + slot_of(d) * SLOT;
@@ -296,8 +239,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
       // axis-0 queues of D(u1,x1), D(u2,x2) at this column (before the
       // barrier: at a segment start they read the oldest slot too)
-      if constexpr (!kBuf) {
-      } else if (t == 0) {
+      if (t == 0) {
 #pragma unroll
         for (int d = 0; d < 5; ++d) {
           SAccW b;
@@ -324,16 +266,9 @@ __global__ void __launch_bounds__(NT, 1)
       }
       __syncthreads();
       if (w == 0) tiled::trace(2);
-      if (tid == 0) {
-        if (issued < total_pos && issued < w + NR + 1) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue_next();   // the next plane, into the oldest slot
-        }
-        if constexpr (kGB) {   // the next step's gradient boxes (other parity:
-                               // every thread is past the step that read them)
-          if (t + 1 < nsteps) issue_gb_tile(gs + 1, k0, j0, i_seg + t + 1);
-          else if (se < S.end) issue_gb(gs + 1, se / nplanes, i_lo + (int)(se % nplanes));
-        }
+      if (tid == 0 && issued < total_pos && issued < w + NR + 1) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_next();   // the next plane, into the oldest slot
       }
 #pragma unroll
       for (int d = 0; d < 5; ++d) a.p[d] = sm + slot_of(d) * SLOT + toff;
@@ -343,14 +278,9 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int f = 0; f < NFIELDS; ++f) r[f] = a.v(f, 0, 0, 0);   // r[RHOE_F] = rho*e
       double R[5];
-      if constexpr (kBuf) {
+      {
         const tiled::TiledLazyProviderT<SAcc12, TK> P{
             k, a, q1, q2, bufs + toff, bu1 + toff, bu2 + (tj + 2) * TK + tk};
-        residual_point<true>(k, P, r, R);
-      } else {
-        mbar_wait(&gbars[gs & 1], (gs >> 1) & 1);
-        const tiled::TiledSSProvider<V == FDNS_RS, SAcc12, TK> P{
-            k, a, q1, q2, bufs + toff, bu1 + toff, bu2 + (tj + 2) * TK + tk, gv};
         residual_point<true>(k, P, r, R);
       }
       if (active) {

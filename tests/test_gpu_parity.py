@@ -405,8 +405,10 @@ def kernel_path():
 def test_tiled_segment_transitions(kernel_path, variant, ctas, path):
     """Force the persistent tiled kernel onto few CTAs so each walks several
     (tile, plane-range) segments; results stay bitwise equal to the
-    one-thread-per-point path.  Path 5 runs SN/SS/RS on the 12-warp kernel
-    (at this size the default picks the 8-warp one)."""
+    one-thread-per-point path.  Path 5 runs SN on the 12-warp kernel (at
+    this size the default picks the 8-warp one)."""
+    if path == 5 and variant != "SN":
+        pytest.skip("kernel path 5 only changes SN")
     npts = (21, 20, 34)
     F = npo.state_from_primitives(npts, CO, np.ones(npts) + 0.01 * np.arange(
         np.prod(npts)).reshape(npts) / np.prod(npts),
@@ -450,14 +452,18 @@ def test_sn_kernel_families_agree(kernel_path, ctas):
 @pytest.mark.parametrize("variant", ["SN", "SS", "BL", "RA"])
 @pytest.mark.parametrize("nranks", [2, 3])
 @pytest.mark.parametrize("split", [False, True])
-def test_slab_decomposition_bitwise_invariant(variant, nranks, split):
+@pytest.mark.parametrize("path", [0, 5])
+def test_slab_decomposition_bitwise_invariant(kernel_path, variant, nranks, split, path):
     """z-slab decomposition emulated on one GPU: each 'rank' owns
     a slab grid (wrap_mask 0b110, so its stage kernels write axis-1/2 ghosts
     only) and the axis-0 ghost planes are copied between the ranks' bundles
     after every stage, as Slab.exchange does over NCCL.  The ranks' kernels
     never wait on each other (the host sequences stage -> exchange), so this
     is a faithful single-GPU emulation.  Fields must equal the one-GPU run
-    bitwise."""
+    bitwise.  Path 5 runs SN on the 12-warp kernel (plane-range launches of
+    the boundary/interior split included)."""
+    if path == 5 and variant != "SN":
+        pytest.skip("kernel path 5 only changes SN")
     n0, n1, n2, h = 24, 16, 20, 2
     npts = (n0, n1, n2)
     F = npo.manufactured(npts, CO)
@@ -465,8 +471,9 @@ def test_slab_decomposition_bitwise_invariant(variant, nranks, split):
     ref = state_from_cons(g1, npo.interior(F[:5], 2))
     scheme = fd.RKScheme(dt=2e-3)
     fd.run(ref, scheme, fd.ResidualEvaluator(g1, C, variant), 2)
-    want = host_cons(ref)
+    want = host_cons(ref)   # one GPU, default kernels
 
+    kernel_path.fdns_set_kernel_path(path)
     slabs = [fd.Slab.partition(n0, r, nranks) for r in range(nranks)]
     grids, states, evs = [], [], []
     for sl in slabs:
