@@ -727,7 +727,13 @@ Launch pick_launch(int ntk, int ntj, int planes, int wrap, int variant, cudaStre
   double best_cost = split_cost(G0, tc, planes, tiled::SPLIT_CONTIGUOUS);
   const double cb = split_cost(G0, tc, planes, tiled::SPLIT_BALANCED);
   if (cb < best_cost - 1e-9) { best_cost = cb; best = {G0, tiled::SPLIT_BALANCED, nullptr}; }
-  for (int64_t G = tiles; G <= G0; ++G) {
+  // tile-aligned splits: one segment (one ramp) per CTA.  Small launches
+  // (few planes, e.g. a slab's boundary planes) may use up to one CTA per
+  // plane step: with G0 = total/4 their CTAs would each walk several short
+  // segments, a ramp apiece (the boundary-first split cost +87% over one
+  // launch at 64^3; tools/split_cost.py)
+  const int64_t Gmax = std::max<int64_t>(G0, std::min<int64_t>(num_sms(), total));
+  for (int64_t G = tiles; G <= Gmax; ++G) {
     const double c = split_cost(G, tc, planes, tiled::SPLIT_ALIGNED);
     if (c < best_cost - 1e-9) { best_cost = c; best = {G, tiled::SPLIT_ALIGNED, nullptr}; }
   }

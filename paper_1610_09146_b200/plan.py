@@ -384,6 +384,25 @@ class ResidualEvaluator:
             int(with_fills), self.problem, _lib.stream_handle()),
             f"stage ({self.plan.name})")
 
+    def stage_boundary(self, inp: torch.Tensor, saved: torch.Tensor,
+                       out: torch.Tensor, coef: float) -> None:
+        """The first half of an overlapped slab stage: the work-array fills
+        and the h planes at each end of the slab, back to back on the
+        launching stream (two small launches; running the second on a side
+        stream measured slower at 64^3 -- the cross-stream join costs more
+        than the launch it overlaps, tools/split_cost.py)."""
+        h = self.grid.halo
+        n = self.grid.local_npoints[0]
+        self.stage_planes(inp, saved, out, coef, 0, h, True)
+        self.stage_planes(inp, saved, out, coef, n - h, n, False)
+
+    def stage_interior(self, inp: torch.Tensor, saved: torch.Tensor,
+                       out: torch.Tensor, coef: float) -> None:
+        """The second half: the planes between the boundary planes."""
+        h = self.grid.halo
+        n = self.grid.local_npoints[0]
+        self.stage_planes(inp, saved, out, coef, h, n - h, False)
+
     def stage_exchanged(self, inp: torch.Tensor, saved: torch.Tensor,
                         out: torch.Tensor, coef: float) -> None:
         """One stage of a z-slab rank with the halo exchange overlapped:
@@ -399,12 +418,11 @@ class ResidualEvaluator:
         main = torch.cuda.current_stream()
         if getattr(self, "_comm", None) is None:
             self._comm = torch.cuda.Stream()
-        self.stage_planes(inp, saved, out, coef, 0, h, True)
-        self.stage_planes(inp, saved, out, coef, n - h, n, False)
+        self.stage_boundary(inp, saved, out, coef)
         self._comm.wait_stream(main)
         with torch.cuda.stream(self._comm):
             slab.exchange(out, h)
-        self.stage_planes(inp, saved, out, coef, h, n - h, False)
+        self.stage_interior(inp, saved, out, coef)
         main.wait_stream(self._comm)
 
 

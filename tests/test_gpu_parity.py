@@ -503,13 +503,10 @@ def test_slab_decomposition_bitwise_invariant(kernel_path, variant, nranks, spli
             coef = scheme.alpha[k] * scheme.dt
             if split:   # the overlapped order of ResidualEvaluator.stage_exchanged
                 for r in range(nranks):
-                    n = slabs[r].local_n0
-                    evs[r].stage_planes(src[k][r], X[r], dst[k][r], coef, 0, h, True)
-                    evs[r].stage_planes(src[k][r], X[r], dst[k][r], coef, n - h, n, False)
+                    evs[r].stage_boundary(src[k][r], X[r], dst[k][r], coef)
                 exchange(dst[k])
                 for r in range(nranks):
-                    n = slabs[r].local_n0
-                    evs[r].stage_planes(src[k][r], X[r], dst[k][r], coef, h, n - h, False)
+                    evs[r].stage_interior(src[k][r], X[r], dst[k][r], coef)
             else:
                 for r in range(nranks):
                     evs[r].stage(src[k][r], X[r], dst[k][r], coef)
