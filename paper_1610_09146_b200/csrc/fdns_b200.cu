@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <map>
 #include <mutex>
 #include <atomic>
@@ -676,32 +677,62 @@ double split_cost(int64_t G, const TileCost& tc, int planes, int mode,
   return worst;
 }
 
-// Cut points of G contiguous ranges of equal weighted cost in tile-major
-// order (each tile: its plane steps times its weight, plus one mid-range
-// ramp).
+// Cut points of G contiguous ranges in tile-major order minimising the
+// largest range cost (plane steps times the tile's weight, plus a mid-range
+// ramp for every tile a range enters after its first): binary search on
+// that cost, each candidate checked by a greedy fill.  (Cutting at equal
+// fractions of the total cost instead rounds each cut on its own and left
+// some CTAs a whole step more than needed: 8 instead of 7 plane steps at
+// 64^3, those CTAs ending ~3 us after the median.)
 std::vector<int64_t> table_cuts(int64_t G, const TileCost& tc, int planes) {
   const int64_t tiles = (int64_t)tc.ntk * tc.ntj;
+  const int64_t total = tiles * planes;
   const double Rm = tiled::RAMP_MID_Q / 4.0;
-  double V = 0;
-  for (int64_t t = 0; t < tiles; ++t) V += planes * tc.weight(t) + Rm;
-  std::vector<int64_t> cuts(G + 1);
-  int64_t t = 0;
-  double acc = 0;   // cost of tiles [0, t)
-  for (int64_t b = 0; b < G; ++b) {
-    const double target = V * (double)b / (double)G;
-    while (t < tiles && acc + planes * tc.weight(t) + Rm <= target) {
-      acc += planes * tc.weight(t) + Rm;
-      ++t;
+  // CTAs the greedy fill needs at max cost C (cut points into *cuts)
+  auto fill = [&](double C, std::vector<int64_t>* cuts) -> int64_t {
+    int64_t ctas = 1;
+    double cur = 0;
+    bool fresh = true;   // the current CTA has no segment yet
+    if (cuts) cuts->assign(1, 0);
+    for (int64_t t = 0; t < tiles; ++t) {
+      const double wt = tc.weight(t);
+      int64_t left = planes;
+      while (left > 0) {
+        const double extra = fresh ? 0.0 : Rm;
+        int64_t fit = (int64_t)std::floor((C - cur - extra) / wt + 1e-9);
+        if (fit <= 0 && fresh) fit = 1;   // C below one step: never stall
+        if (fit <= 0) {
+          ++ctas; cur = 0; fresh = true;
+          if (cuts) cuts->push_back(t * planes + (planes - left));
+          continue;
+        }
+        const int64_t take = std::min(fit, left);
+        cur += extra + take * wt;
+        fresh = false;
+        left -= take;
+        if (left > 0) {
+          ++ctas; cur = 0; fresh = true;
+          if (cuts) cuts->push_back(t * planes + (planes - left));
+        }
+      }
     }
-    int64_t p = 0;
-    if (t < tiles) {
-      const double off = target - acc - Rm;
-      p = off > 0 ? (int64_t)(off / tc.weight(t) + 0.5) : 0;
-      p = std::min<int64_t>(p, planes);
-    }
-    cuts[b] = std::min<int64_t>(t * planes + p, tiles * planes);
+    return ctas;
+  };
+  double wmax = 0, V = 0;
+  for (int64_t t = 0; t < tiles; ++t) {
+    wmax = std::max(wmax, tc.weight(t));
+    V += planes * tc.weight(t);
   }
-  cuts[G] = tiles * planes;
+  double lo = std::max(V / (double)G, wmax), hi = lo + 2 * wmax + Rm;
+  while (fill(hi, nullptr) > G) hi = 2 * hi;
+  for (int it = 0; it < 60 && hi - lo > 1e-6; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (fill(mid, nullptr) <= G) hi = mid; else lo = mid;
+  }
+  std::vector<int64_t> cuts;
+  fill(hi, &cuts);
+  cuts.resize(G + 1, total);   // unused CTAs get empty ranges
+  cuts[G] = total;
   for (int64_t b = 1; b <= G; ++b) cuts[b] = std::max(cuts[b], cuts[b - 1]);
   return cuts;
 }

@@ -18,7 +18,9 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 g = fd.make_grid((n,) * 3, (2 * np.pi,) * 3)
 c = fd.PhysicalConstants()
-configs = [(u, k) for u in ("ce", "sm") for k in (1, 2, 5)]
+ks = tuple(int(x) for x in os.environ.get("E2E_CHUNKS", "1,2,5").split(","))
+ups = tuple(os.environ.get("E2E_UPLOAD", "ce,sm").split(","))
+configs = [(u, k) for u in ups for k in ks]
 res = {cfg: [] for cfg in configs}
 for rnd in range(3):
     for up, k in configs:
