@@ -740,7 +740,7 @@ std::vector<int64_t> table_cuts(int64_t G, const TileCost& tc, int planes) {
 struct Launch { int64_t ctas; int aligned; const int64_t* cuts; };
 
 Launch pick_launch(int ntk, int ntj, int planes, int wrap, int variant, cudaStream_t s,
-                   bool allow_table = true) {
+                   bool allow_table = true, int ctas_per_sm = 1) {
   const int64_t tiles = (int64_t)ntk * ntj;
   const int64_t total = tiles * planes;
   if (g_tiled_ctas > 0)
@@ -753,7 +753,8 @@ Launch pick_launch(int ntk, int ntj, int planes, int wrap, int variant, cudaStre
   const Key key{ntk, ntj, planes, (wrap & 6) | (allow_table ? 8 : 0), variant};
   const auto hit = cache.find(key);
   if (hit != cache.end()) return hit->second;
-  const int64_t G0 = std::max<int64_t>(1, std::min<int64_t>(num_sms(), total / 4));
+  const int64_t sms = (int64_t)num_sms() * ctas_per_sm;
+  const int64_t G0 = std::max<int64_t>(1, std::min<int64_t>(sms, total / 4));
   Launch best{G0, tiled::SPLIT_CONTIGUOUS, nullptr};
   double best_cost = split_cost(G0, tc, planes, tiled::SPLIT_CONTIGUOUS);
   const double cb = split_cost(G0, tc, planes, tiled::SPLIT_BALANCED);
@@ -763,7 +764,7 @@ Launch pick_launch(int ntk, int ntj, int planes, int wrap, int variant, cudaStre
   // plane step: with G0 = total/4 their CTAs would each walk several short
   // segments, a ramp apiece (the boundary-first split cost +87% over one
   // launch at 64^3; tools/split_cost.py)
-  const int64_t Gmax = std::max<int64_t>(G0, std::min<int64_t>(num_sms(), total));
+  const int64_t Gmax = std::max<int64_t>(G0, std::min<int64_t>(sms, total));
   for (int64_t G = tiles; G <= Gmax; ++G) {
     const double c = split_cost(G, tc, planes, tiled::SPLIT_ALIGNED);
     if (c < best_cost - 1e-9) { best_cost = c; best = {G, tiled::SPLIT_ALIGNED, nullptr}; }
@@ -838,28 +839,33 @@ inline bool use_t12(const Geom& g) {
 }
 
 // The 12-warp SN stage kernel (fdns_tiled12.cuh): its own 36 x 16 plane box.
-template <int MODE>
+template <int MODE, int TJ_ = 12>
 int launch_t12(const double* in, const double* saved, double* out, const Coef& k, const Geom& g,
                double coef, int wrap, int i_lo, int i_hi, cudaStream_t s) {
+  using L = t12::Lay<TJ_>;
   CUtensorMap m, ms;
-  if (!plane_map(&m, in, g, t12::PJ)) return fail("plane tensor map");
+  if (!plane_map(&m, in, g, L::PJ)) return fail("plane tensor map");
   ms = m;
   int pf = 0;
   if constexpr (MODE == 1)
-    pf = (g_prefetch_saved && saved != in && saved_map(&ms, saved, g, t12::TJ)) ? 1 : 0;
+    pf = (g_prefetch_saved && saved != in && saved_map(&ms, saved, g, L::TJ)) ? 1 : 0;
   static std::once_flag attr;
   std::call_once(attr, [] {
-    cudaFuncSetAttribute(t12::k_stage_t12<FDNS_SN, MODE>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, t12::SMEM_BYTES);
+    cudaFuncSetAttribute(t12::k_stage_t12<FDNS_SN, MODE, TJ_>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_BYTES);
+    if (L::MINB > 1)
+      cudaFuncSetAttribute(t12::k_stage_t12<FDNS_SN, MODE, TJ_>,
+                           cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   });
-  const int ntk = (g.n2 + t12::TK - 1) / t12::TK;
-  const int ntj = (g.n1 + t12::TJ - 1) / t12::TJ;
+  const int ntk = (g.n2 + L::TK - 1) / L::TK;
+  const int ntj = (g.n1 + L::TJ - 1) / L::TJ;
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
-  const Launch L = pick_launch(ntk, ntj, nplanes, wrap, FDNS_SN | 0x100, s);
-  launch_pdl(t12::k_stage_t12<FDNS_SN, MODE>, dim3((unsigned)L.ctas), dim3(t12::NT),
-             t12::SMEM_BYTES, s, m, ms, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes,
-             L.aligned, pf, L.cuts);
+  const Launch Lc = pick_launch(ntk, ntj, nplanes, wrap, FDNS_SN | 0x100 | (TJ_ << 12), s, true,
+                                L::MINB);
+  launch_pdl(t12::k_stage_t12<FDNS_SN, MODE, TJ_>, dim3((unsigned)Lc.ctas), dim3(L::NT),
+             L::SMEM_BYTES, s, m, ms, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes,
+             Lc.aligned, pf, Lc.cuts);
   return 0;
 }
 

@@ -36,28 +36,41 @@ using tiled::Segments;
 using tiled::tma_load_plane;
 using tiled::tma_prefetch_l2;
 
-constexpr int TK = 32, TJ = 12, NT = TK * TJ;
-constexpr int PK = TK + 4, PJ = TJ + 4;
-constexpr int PLANE = PK * PJ;
 constexpr int NSF = 9;                  // staged fields: rho, rhou0..2, rho*e, u0..2, T
 constexpr int SF_T = 8;                 // slot index of T
-constexpr int SLOT = NSF * PLANE;
 constexpr int NLOAD = 8;                // TMA-loaded fields (rho..u2)
-constexpr uint32_t LOAD_BYTES = NLOAD * PLANE * 8;
 constexpr int NR = 5;                   // ring depth = the stencil window
-constexpr int BU1_N = TJ * PK;          // D(u1,x1): tile rows, all box columns
-constexpr int BU2_N = PJ * TK;          // D(u2,x2): all box rows, tile columns (pitch TK)
-constexpr int BUFSET = PLANE + BU1_N + BU2_N;
-constexpr int SMEM_BYTES = NR * SLOT * 8 + 2 * BUFSET * 8 + 64;
-static_assert(SMEM_BYTES <= 232448, "12-warp tile exceeds the 227 KB shared-memory limit");
-static_assert(PLANE <= 2 * NT && BU1_N <= 2 * NT && BU2_N <= 2 * NT,
-              "per-plane items: at most two per thread");
+
+// Tile layout: a 32 x TJ column tile, one thread per point.  TJ = 12: one
+// 384-thread CTA per SM (the default SN kernel on grids whose rows fit).
+// (TJ = 4 -- 128-thread CTAs, two per SM, their step barriers independent
+// -- measured 2-3% slower than the 8-warp kernel at 64^3-256^3: the halo
+// overhead of a 36 x 8 box outweighs the desynchronised warps.)
+template <int TJ_>
+struct Lay {
+  static constexpr int TK = 32, TJ = TJ_, NT = TK * TJ;
+  static constexpr int PK = TK + 4, PJ = TJ + 4;
+  static constexpr int PLANE = PK * PJ;
+  static constexpr int SLOT = NSF * PLANE;
+  static constexpr uint32_t LOAD_BYTES = NLOAD * PLANE * 8;
+  static constexpr int BU1_N = TJ * PK;   // D(u1,x1): tile rows, all box columns
+  static constexpr int BU2_N = PJ * TK;   // D(u2,x2): all box rows, tile columns (pitch TK)
+  static constexpr int BUFSET = PLANE + BU1_N + BU2_N;
+  static constexpr int SMEM_BYTES = NR * SLOT * 8 + 2 * BUFSET * 8 + 64;
+  static constexpr int MINB = TJ_ <= 4 ? 2 : 1;   // CTAs per SM
+  static_assert(MINB * (SMEM_BYTES + 1024) <= 233472, "tile exceeds shared memory");
+};
+// the default (12-warp) layout's names, used by the host launcher
+using L12 = Lay<12>;
+constexpr int TK = L12::TK, TJ = L12::TJ, NT = L12::NT, PK = L12::PK, PJ = L12::PJ;
+constexpr int SMEM_BYTES = L12::SMEM_BYTES;
 
 __device__ __forceinline__ constexpr int sfield(int f) { return f == TF ? SF_T : f; }
 
 // Accessor of the staged window.  Taps at axis-0 offset -2 come from the
 // registers m2 (read before the step barrier: that slot is being refilled by
 // then); the SN provider only taps the oldest plane at its own column.
+template <class L>
 struct SAcc12 {
   static constexpr bool kInternalEnergy = true;
   static constexpr bool kMaskTaps = true;
@@ -67,7 +80,7 @@ struct SAcc12 {
   __device__ __forceinline__ double raw(int f, int di, int dj, int dk) const {
     const int sf = sfield(f);
     if (di == -2) return m2[sf];
-    return p[di + 2][sf * PLANE + dj * PK + dk];
+    return p[di + 2][sf * L::PLANE + dj * L::PK + dk];
   }
   __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
     if (f == PF) return gm1 * raw(RHOE_F, di, dj, dk);   // p = gm1 * rho*e
@@ -77,19 +90,22 @@ struct SAcc12 {
 
 // Accessor over all five window planes in shared memory (the centre-plane
 // buffers, before the step barrier).
+template <class L>
 struct SAccW {
   static constexpr bool kInternalEnergy = true;
   static constexpr bool kMaskTaps = true;
   const double* p[5];
   __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
-    return p[di + 2][sfield(f) * PLANE + dj * PK + dk];
+    return p[di + 2][sfield(f) * L::PLANE + dj * L::PK + dk];
   }
 };
 
 // Arrival conversion (fdns_tiled.cuh:stage_arrival without the p field).
+template <class L>
 __device__ __forceinline__ void stage_arrival(const Coef& k, double* slot, int tid) {
+  constexpr int PLANE = L::PLANE;
 #pragma unroll 1
-  for (int x = tid; x < PLANE; x += NT) {
+  for (int x = tid; x < PLANE; x += L::NT) {
     const double rho = slot[RHO * PLANE + x];
     const double e = slot[RHOE_F * PLANE + x] -
                      0.5 * (slot[RU0 * PLANE + x] * slot[U0 * PLANE + x] +
@@ -101,13 +117,19 @@ __device__ __forceinline__ void stage_arrival(const Coef& k, double* slot, int t
   }
 }
 
-template <int V, int MODE>
-__global__ void __launch_bounds__(NT, 1)
+template <int V, int MODE, int TJ_ = 12>
+__global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
     k_stage_t12(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tsv,
                 const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
                 int64_t total_steps, int wrap_mask, int i_lo, int nplanes, int split,
                 int pf_saved, const int64_t* __restrict__ cuts) {
   static_assert(V == FDNS_SN, "12-warp kernel: SN");
+  using L = Lay<TJ_>;
+  constexpr int TK = L::TK, TJ = L::TJ, NT = L::NT, PK = L::PK, PLANE = L::PLANE;
+  constexpr int SLOT = L::SLOT, BU1_N = L::BU1_N, BU2_N = L::BU2_N, BUFSET = L::BUFSET;
+  constexpr uint32_t LOAD_BYTES = L::LOAD_BYTES;
+  using SAcc12 = t12::SAcc12<L>;
+  using SAccW = t12::SAccW<L>;
   extern __shared__ __align__(128) double sm[];
   double* bufs0 = sm + NR * SLOT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NR * SLOT + 2 * BUFSET);
@@ -193,11 +215,11 @@ __global__ void __launch_bounds__(NT, 1)
       if (t == 0) {
         for (int d = 0; d < 5; ++d) {
           mbar_wait(&bars[slot_of(d)], ((w + d) / NR) & 1);
-          stage_arrival(k, sm + slot_of(d) * SLOT, tid);
+          stage_arrival<L>(k, sm + slot_of(d) * SLOT, tid);
         }
       } else {
         mbar_wait(&bars[slot_of(4)], ((w + 4) / NR) & 1);
-        stage_arrival(k, sm + slot_of(4) * SLOT, tid);
+        stage_arrival<L>(k, sm + slot_of(4) * SLOT, tid);
       }
       double* bufs = bufs0 + (w & 1) * BUFSET;
       double* bu1 = bufs + PLANE - 2 * PK;   // row 2 of the box at offset PLANE
@@ -206,6 +228,7 @@ __global__ void __launch_bounds__(NT, 1)
         const double* base[5];
 #pragma unroll
         for (int d = 0; d < 5; ++d) base[d] = sm + slot_of(d) * SLOT;
+        if constexpr (TJ == 12) {
         // items past the first NT of each buffer go to the threads that
         // converted only one point of the new plane (tid >= PLANE - NT), so
         // no warp carries much more than the average (max 9 vs 12 units,
@@ -230,6 +253,29 @@ __global__ void __launch_bounds__(NT, 1)
           }
           const int y2 = m == 0 ? tid : tid + 144;   // D(u2,x2), cols 2..TK+1
           if (m == 0 || (tid >= 240 && y2 < BU2_N)) {
+            const int row = y2 / TK, col = y2 % TK;
+            SAccW b;
+            b.p[2] = base[2] + row * PK + 2 + col;
+            bu2[y2] = d1<2, E_FIELD, U2, 0>(k, b);
+          }
+        }
+        } else {
+#pragma unroll 1
+          for (int x0 = tid; x0 < PLANE; x0 += NT) {   // D(u0,x0), whole box
+            SAccW b;
+#pragma unroll
+            for (int d = 0; d < 5; ++d) b.p[d] = base[d] + x0;
+            bufs[x0] = d1<0, E_FIELD, U0, 0>(k, b);
+          }
+#pragma unroll 1
+          for (int y1 = tid; y1 < BU1_N; y1 += NT) {   // D(u1,x1), rows 2..TJ+1
+            const int pos = 2 * PK + y1;
+            SAccW b;
+            b.p[2] = base[2] + pos;
+            bu1[pos] = d1<1, E_FIELD, U1, 0>(k, b);
+          }
+#pragma unroll 1
+          for (int y2 = tid; y2 < BU2_N; y2 += NT) {   // D(u2,x2), cols 2..TK+1
             const int row = y2 / TK, col = y2 % TK;
             SAccW b;
             b.p[2] = base[2] + row * PK + 2 + col;
