@@ -399,16 +399,13 @@ def kernel_path():
     lib.fdns_set_tiled_grid(0)
 
 
-@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("variant,path", [(v, 0) for v in VARIANTS] + [("SN", 5)])
 @pytest.mark.parametrize("ctas", [3, 7, 13])
-@pytest.mark.parametrize("path", [0, 5])
 def test_tiled_segment_transitions(kernel_path, variant, ctas, path):
     """Force the persistent tiled kernel onto few CTAs so each walks several
     (tile, plane-range) segments; results stay bitwise equal to the
     one-thread-per-point path.  Path 5 runs SN on the 12-warp kernel (at
     this size the default picks the 8-warp one)."""
-    if path != 0 and variant != "SN":
-        pytest.skip("kernel path 5 only changes SN")
     npts = (21, 20, 34)
     F = npo.state_from_primitives(npts, CO, np.ones(npts) + 0.01 * np.arange(
         np.prod(npts)).reshape(npts) / np.prod(npts),
@@ -449,10 +446,10 @@ def test_sn_kernel_families_agree(kernel_path, ctas):
 
 
 # ------------------------------------------------ decomposition invariance
-@pytest.mark.parametrize("variant", ["SN", "SS", "BL", "RA"])
+@pytest.mark.parametrize("variant,path", [("SN", 0), ("SS", 0), ("BL", 0), ("RA", 0),
+                                          ("SN", 5)])
 @pytest.mark.parametrize("nranks", [2, 3])
 @pytest.mark.parametrize("split", [False, True])
-@pytest.mark.parametrize("path", [0, 5])
 def test_slab_decomposition_bitwise_invariant(kernel_path, variant, nranks, split, path):
     """z-slab decomposition emulated on one GPU: each 'rank' owns
     a slab grid (wrap_mask 0b110, so its stage kernels write axis-1/2 ghosts
@@ -462,8 +459,6 @@ def test_slab_decomposition_bitwise_invariant(kernel_path, variant, nranks, spli
     is a faithful single-GPU emulation.  Fields must equal the one-GPU run
     bitwise.  Path 5 runs SN on the 12-warp kernel (plane-range launches of
     the boundary/interior split included)."""
-    if path == 5 and variant != "SN":
-        pytest.skip("kernel path 5 only changes SN")
     n0, n1, n2, h = 24, 16, 20, 2
     npts = (n0, n1, n2)
     F = npo.manufactured(npts, CO)
