@@ -94,6 +94,15 @@ int validate(const fdns_problem* pb) {
 // ---------------------------------------------------------------------------
 // Primitives over the full padded bundle
 // ---------------------------------------------------------------------------
+// Entry of a kernel launched with programmatic dependent launch: wait for
+// the preceding kernel's writes before any global access, then let the
+// next kernel in the stream be scheduled as this grid's CTAs retire.  (A
+// no-op pair when launched without the attribute.)
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+
 __global__ void k_primitives(double* __restrict__ F, Coef k, int64_t fs) {
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < fs;
        c += (int64_t)gridDim.x * blockDim.x) {
@@ -180,6 +189,7 @@ __global__ void __launch_bounds__(256) k_residual(const double* __restrict__ in,
                                                   const double* __restrict__ work, Coef k,
                                                   Geom g, double coef, int wrap_mask,
                                                   int i_lo) {
+  pdl_entry();
   const int kk = point_k(g);
   const int jj = blockIdx.y * blockDim.y + threadIdx.y;
   const int ii = blockIdx.z + i_lo;
@@ -232,6 +242,7 @@ __device__ __forceinline__ void fill_axis_all(const Coef& k, const GAcc& a,
 // value is the same expression, so bitwise equal).
 __global__ void __launch_bounds__(256) k_fill_bl_all(const double* __restrict__ in,
                                                      double* __restrict__ wa, Coef k, Geom g) {
+  pdl_entry();
   const int kk = point_k(g);
   const int jj = blockIdx.y * blockDim.y + threadIdx.y;
   const int ii = blockIdx.z;
@@ -283,6 +294,7 @@ __device__ __forceinline__ void diag_ghost_point(const double* __restrict__ in,
 __global__ void k_diag_ghost(const double* __restrict__ in, double* __restrict__ d0,
                              double* __restrict__ d1p, double* __restrict__ d2p, Coef k, Geom g,
                              int64_t f0, int64_t f1, int64_t f2) {
+  pdl_entry();
   const int64_t total = f0 + f1 + f2;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -294,6 +306,7 @@ __global__ void k_diag_ghost(const double* __restrict__ in, double* __restrict__
 
 // BL mixed fills: outer derivative of the stored inner arrays (plan.py:380-382).
 __global__ void __launch_bounds__(256, 4) k_fill_cross(double* __restrict__ wa, Coef k, Geom g) {
+  pdl_entry();
   const int kk = point_k(g);
   const int jj = blockIdx.y * blockDim.y + threadIdx.y;
   const int ii = blockIdx.z;
@@ -318,6 +331,7 @@ __global__ void __launch_bounds__(256) k_grad_ss_all(const double* __restrict__ 
                                                      double* __restrict__ ws, Coef k, Geom g,
                                                      int64_t nint, int64_t f0, int64_t f1,
                                                      int64_t f2) {
+  pdl_entry();
   const int64_t total = nint + f0 + f1 + f2;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -368,6 +382,7 @@ __global__ void __launch_bounds__(256) k_derivative(const double* __restrict__ f
 __global__ void __launch_bounds__(256) k_grad_ss_interior(const double* __restrict__ in,
                                                           double* __restrict__ ws, Coef k,
                                                           Geom g) {
+  pdl_entry();
   const int kk = point_k(g);
   const int jj = blockIdx.y * blockDim.y + threadIdx.y;
   const int ii = blockIdx.z;
@@ -917,11 +932,11 @@ int launch_residual(int variant, const double* in, const double* saved, double* 
   dim3 grd = point_grid(g, blk);
   grd.z = i_hi - i_lo;
   switch (variant) {
-    case FDNS_BL: k_residual<FDNS_BL, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap, i_lo); break;
-    case FDNS_RA: k_residual<FDNS_RA, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap, i_lo); break;
-    case FDNS_RS: k_residual<FDNS_RS, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap, i_lo); break;
-    case FDNS_SN: k_residual<FDNS_SN, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap, i_lo); break;
-    case FDNS_SS: k_residual<FDNS_SS, MODE><<<grd, blk, 0, s>>>(in, saved, out, work, k, g, coef, wrap, i_lo); break;
+    case FDNS_BL: launch_pdl(k_residual<FDNS_BL, MODE>, grd, blk, 0, s, in, saved, out, work, k, g, coef, wrap, i_lo); break;
+    case FDNS_RA: launch_pdl(k_residual<FDNS_RA, MODE>, grd, blk, 0, s, in, saved, out, work, k, g, coef, wrap, i_lo); break;
+    case FDNS_RS: launch_pdl(k_residual<FDNS_RS, MODE>, grd, blk, 0, s, in, saved, out, work, k, g, coef, wrap, i_lo); break;
+    case FDNS_SN: launch_pdl(k_residual<FDNS_SN, MODE>, grd, blk, 0, s, in, saved, out, work, k, g, coef, wrap, i_lo); break;
+    case FDNS_SS: launch_pdl(k_residual<FDNS_SS, MODE>, grd, blk, 0, s, in, saved, out, work, k, g, coef, wrap, i_lo); break;
     default: return fail("unknown variant");
   }
   count();
@@ -936,21 +951,26 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
                  cudaStream_t s) {
   const dim3 blk(32, 8, 1);
   const dim3 grd = point_grid(g, blk);
-  auto ghosts = [&](double* d0, double* d1p, double* d2p) {
+  // programmatic dependent launch for the fills: BL's chain and the one-
+  // launch SS/RS fill (+1.4-1.8% BL/SS/RS steps at 64^3); the 3-D SS/RS
+  // fill path keeps plain launches (with PDL its steps were 5-8% slower at
+  // 128^3-256^3)
+  auto ghosts = [&](double* d0, double* d1p, double* d2p, bool pdl) {
     const int h = g.h;
     const int64_t f0 = (int64_t)g.n0 * (2 * h * (g.n2 + 2 * h) + (int64_t)g.n1 * 2 * h);
     const int64_t f1 = (int64_t)g.n1 * (2 * h * (g.n2 + 2 * h) + (int64_t)g.n0 * 2 * h);
     const int64_t f2 = (int64_t)g.n2 * (2 * h * (g.n1 + 2 * h) + (int64_t)g.n0 * 2 * h);
     const int nb = (int)std::min<int64_t>((f0 + f1 + f2 + 255) / 256, 148 * 8);
-    k_diag_ghost<<<nb, 256, 0, s>>>(in, d0, d1p, d2p, k, g, f0, f1, f2);
+    if (pdl) launch_pdl(k_diag_ghost, dim3(nb), dim3(256), 0, s, in, d0, d1p, d2p, k, g, f0, f1, f2);
+    else k_diag_ghost<<<nb, 256, 0, s>>>(in, d0, d1p, d2p, k, g, f0, f1, f2);
   };
   if (variant == FDNS_BL) {
     // (a TMA-staged fill, k_stage_tiled<BL, 2>, measured 1.6x slower at
     // 256^3: 8 warps/SM cannot keep 54 store streams in flight)
-    k_fill_bl_all<<<grd, blk, 0, s>>>(in, work, k, g);
+    launch_pdl(k_fill_bl_all, grd, blk, 0, s, in, work, k, g);
     ghosts(work + slot(0, S_U + 0) * g.fs, work + slot(1, S_U + 1) * g.fs,
-           work + slot(2, S_U + 2) * g.fs);
-    k_fill_cross<<<grd, blk, 0, s>>>(work, k, g);
+           work + slot(2, S_U + 2) * g.fs, true);
+    launch_pdl(k_fill_cross, grd, blk, 0, s, work, k, g);
     count(3);
     return check_launch("BL fills");
   }
@@ -959,7 +979,7 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
   // (its single launch wins at 64^3: -4% otherwise)
   if ((variant == FDNS_SS || variant == FDNS_RS) && g_ss_fill_3d && g.n2 >= 128) {
     k_grad_ss_interior<<<grd, blk, 0, s>>>(in, work, k, g);
-    ghosts(work + 0 * g.fs, work + 4 * g.fs, work + 8 * g.fs);
+    ghosts(work + 0 * g.fs, work + 4 * g.fs, work + 8 * g.fs, false);
     count(2);
     return check_launch("SS fills");
   }
@@ -971,7 +991,7 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
       const int64_t f1 = (int64_t)g.n1 * (2 * h * (g.n2 + 2 * h) + (int64_t)g.n0 * 2 * h);
       const int64_t f2 = (int64_t)g.n2 * (2 * h * (g.n1 + 2 * h) + (int64_t)g.n0 * 2 * h);
       const int nb = (int)std::min<int64_t>((nint + f0 + f1 + f2 + 255) / 256, 148 * 16);
-      k_grad_ss_all<<<nb, 256, 0, s>>>(in, work, k, g, nint, f0, f1, f2);
+      launch_pdl(k_grad_ss_all, dim3(nb), dim3(256), 0, s, in, work, k, g, nint, f0, f1, f2);
     }
     count(1);
     return check_launch("SS fills");
