@@ -96,6 +96,30 @@ int32_t fdns_stage(int32_t variant, const double* in, const double* saved,
                    double* out, double* work, double coef, int32_t wrap_mask,
                    const fdns_problem* pb, void* stream);
 
+/* One whole RK3 iteration (advance_iteration, timeloop.py:88-94) of a
+ * periodic one-GPU state in ONE launch: stage 0 reads X and writes Y, stage 1
+ * reads Y and writes Z, stage 2 reads Z and writes X in place (saved state X
+ * throughout, so the save_state copy of timeloop.py:59-61 disappears);
+ * coefs[k] = alpha[k]*dt.  Between stages every CTA waits only for the CTAs
+ * that wrote its stencil neighbourhood (no grid-wide barrier, no launch
+ * gap).  Bitwise equal to three fdns_stage calls.  `sync` is
+ * fdns_iteration_sync_words() uint32 words, zeroed once by the caller and
+ * reused by every later call on the same stream.  Supported for SN (8-warp
+ * tiled kernel) and RA on grids tiled exactly by 32 x 8 columns with
+ * wrap_mask 0b111 (fdns_iteration_supported); otherwise it fails and the
+ * caller uses fdns_stage.  Disabled unless fdns_set_fused_iteration(1). */
+int32_t fdns_iteration(int32_t variant, double* X, double* Y, double* Z,
+                       uint32_t* sync, const double* coefs, int32_t wrap_mask,
+                       const fdns_problem* pb, void* stream);
+int32_t fdns_iteration_supported(int32_t variant, int32_t wrap_mask,
+                                 const fdns_problem* pb);
+int32_t fdns_iteration_sync_words(void);
+/* Enable or disable (default; FDNS_FUSED_ITERATION=1 enables) the one-launch
+ * iteration; returns the previous setting.  Off by default because the
+ * inter-stage memory-flag hand-off measured slower than three programmatic
+ * (PDL) launches -- see DESIGN.md 3.4. */
+int32_t fdns_set_fused_iteration(int32_t enabled);
+
 /* The fused stage restricted to local axis-0 planes [i_lo, i_hi) (interior
  * indices); work-array fills over the whole slab first when with_fills.  A
  * z-slab rank updates its 2h boundary planes, starts the halo exchange on a

@@ -841,7 +841,149 @@ int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, 
   const Launch L = pick_launch(ntk, ntj, nplanes, wrap, V, s);
   launch_pdl(tiled::k_stage_tiled<V, MODE, LAZY>, dim3((unsigned)L.ctas), dim3(tiled::NT), smem, s,
              m, mg, ms, mp, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes,
-             L.aligned, pf, L.cuts);
+             L.aligned, pf, L.cuts, m, m, tiled::FusedArgs{});
+  return 0;
+}
+
+// Fused RK3 iteration (SN 8-warp / RA tiled kernel, one periodic GPU): one
+// cooperative launch runs the three stages X -> Y -> Z -> X with per-CTA
+// neighbourhood waits between them (fdns_tiled.cuh: FusedArgs).  Same split
+// and same per-point arithmetic as three fdns_stage launches, so bitwise
+// equal to them.
+inline bool use_t12(const Geom& g);
+// Off by default: bitwise equal, but measured slower than three PDL launches
+// (SN 64^3: 94.4 vs 90.1 us per step; RA 128^3: 830 vs 818 us): the
+// memory-flag hand-off between stages (publisher fence + polled L2 flags +
+// acquire fence) takes ~2-4 us after the last neighbour finishes, more than
+// the ~1.2 us programmatic-launch gap it replaces (tools/trace_fused.py,
+// DESIGN.md 3.4).  FDNS_FUSED_ITERATION=1 or fdns_set_fused_iteration(1).
+bool g_fused_iteration = std::getenv("FDNS_FUSED_ITERATION") != nullptr;
+
+bool iteration_supported(int variant, int wrap, const Geom& g) {
+  if (!g_fused_iteration || wrap != 7 || g_tiled_ctas > 0) return false;
+  if (g.n2 % tiled::TK != 0 || g.n1 % tiled::TJ != 0 || g.h != 2) return false;
+  if (((g.n2 + 2 * g.h) * 8) % 16 != 0) return false;   // TMA row pitch
+  if (variant == FDNS_RA) return g_kernel_path == 0;
+  if (variant == FDNS_SN)
+    return g_kernel_path == 2 || (g_kernel_path == 0 && !use_t12(g));
+  return false;
+}
+
+// Dependency lists of a fused iteration (device buffer, cached per
+// geometry/split): CTA b waits, before stage s > 0, for every other CTA
+// owning a (tile, plane) step its TMA boxes read -- the 3 x 3 torus
+// neighbourhood of each of its tiles, planes -2..+2 around each segment,
+// periodic along axis 0.  Layout: [G+1] offsets (relative to the array
+// start), then the CTA ids.
+const int* fused_deps(int ntk, int ntj, int planes, int variant, const Launch& L,
+                      bool may_alloc) {
+  using Key = std::tuple<int, int, int, int, int64_t, int>;
+  static std::map<Key, int*> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  const Key key{ntk, ntj, planes, variant, L.ctas, L.aligned};
+  const auto hit = cache.find(key);
+  if (hit != cache.end()) return hit->second;
+  if (!may_alloc) return nullptr;   // never cudaMalloc inside a graph capture
+  const int64_t G = L.ctas;
+  const int64_t total = (int64_t)ntk * ntj * planes;
+  std::vector<int64_t> cuts;
+  if (L.aligned == tiled::SPLIT_TABLE) {
+    const TileCost tc{ntk, ntj, true, true, edge_scale(variant)};
+    cuts = table_cuts(G, tc, planes);
+  }
+  std::vector<int64_t> beg(G), end(G);
+  for (int64_t b = 0; b < G; ++b) {
+    const tiled::Segments S = tiled::Segments::partition(b, G, total, planes, L.aligned,
+                                                         cuts.empty() ? nullptr : cuts.data());
+    beg[b] = S.beg;
+    end[b] = S.end;
+  }
+  auto owner = [&](int64_t x) {   // largest b with beg[b] <= x
+    return (int64_t)(std::upper_bound(beg.begin(), beg.end(), x) - beg.begin()) - 1;
+  };
+  std::vector<int> out(G + 1, 0);
+  std::vector<int> ids;
+  for (int64_t b = 0; b < G; ++b) {
+    out[b] = (int)(G + 1 + ids.size());
+    std::vector<int> mine;
+    const tiled::Segments S{beg[b], end[b], planes};
+    for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) {
+      const int64_t se = S.seg_end(x), tile = x / planes;
+      const int kt = (int)(tile % ntk), jt = (int)(tile / ntk);
+      const int p0 = (int)(x % planes) - 2, p1 = (int)((se - 1) % planes) + 2;
+      for (int dj = -1; dj <= 1; ++dj)
+        for (int dk = -1; dk <= 1; ++dk) {
+          const int64_t tn = (int64_t)((jt + dj + ntj) % ntj) * ntk + (kt + dk + ntk) % ntk;
+          auto add = [&](int a, int c) {   // planes [a, c] of tile tn
+            for (int64_t o = owner(tn * planes + a); o <= owner(tn * planes + c); ++o)
+              if (o != b && beg[o] < end[o]) mine.push_back((int)o);
+          };
+          if (p1 - p0 + 1 >= planes) add(0, planes - 1);
+          else if (p0 < 0) { add(p0 + planes, planes - 1); add(0, p1); }
+          else if (p1 >= planes) { add(p0, planes - 1); add(0, p1 - planes); }
+          else add(p0, p1);
+        }
+    }
+    std::sort(mine.begin(), mine.end());
+    mine.erase(std::unique(mine.begin(), mine.end()), mine.end());
+    ids.insert(ids.end(), mine.begin(), mine.end());
+  }
+  out[G] = (int)(G + 1 + ids.size());
+  out.insert(out.end(), ids.begin(), ids.end());
+  int* d = nullptr;
+  if (cudaMalloc(&d, out.size() * sizeof(int)) != cudaSuccess ||
+      cudaMemcpy(d, out.data(), out.size() * sizeof(int), cudaMemcpyHostToDevice) !=
+          cudaSuccess) {
+    cudaGetLastError();
+    if (d) cudaFree(d);
+    return nullptr;
+  }
+  cache[key] = d;
+  return d;
+}
+
+template <int V>
+int launch_iteration_v(double* X, double* Y, double* Z, unsigned* sync, const double* coefs,
+                       const Coef& k, const Geom& g, cudaStream_t s) {
+  constexpr int smem = V == FDNS_SN ? tiled::SMEM_BYTES_SN : tiled::SMEM_BYTES;
+  CUtensorMap m0, m1, m2, ms;
+  if (!plane_map(&m0, X, g) || !plane_map(&m1, Y, g) || !plane_map(&m2, Z, g))
+    return fail("plane tensor map");
+  ms = m0;
+  const int pf = (g_prefetch_saved && saved_map(&ms, X, g)) ? 1 : 0;
+  static std::once_flag attr;
+  std::call_once(attr, [] {
+    cudaFuncSetAttribute(tiled::k_stage_tiled<V, 1, true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
+  const int ntk = g.n2 / tiled::TK, ntj = g.n1 / tiled::TJ;
+  const int64_t total = (int64_t)ntk * ntj * g.n0;
+  const Launch L = pick_launch(ntk, ntj, g.n0, 7, V, s);
+  if (L.ctas > num_sms() || L.ctas > tiled::FUSED_SYNC_WORDS - 2)
+    return fail("fused iteration: more CTAs than SMs");
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  const int* deps = fused_deps(ntk, ntj, g.n0, V, L, cs == cudaStreamCaptureStatusNone);
+  if (!deps) return fail("fused iteration: dependency lists unavailable "
+                         "(allocated on the first eager call, not during graph capture)");
+  const tiled::FusedArgs fa{Z, X, coefs[1], coefs[2], sync, deps};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)L.ctas);
+  cfg.blockDim = dim3(tiled::NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;   // every CTA co-resident (they wait on each other)
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  static const bool coop = std::getenv("FDNS_FUSED_NOCOOP") == nullptr;   // A/B only
+  cfg.numAttrs = coop ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(
+      &cfg, tiled::k_stage_tiled<V, 1, true, true>, m0, m0, ms, m0, (const double*)nullptr,
+      (const double*)X, Y, k, g, coefs[0], ntk, total, 7, 0, g.n0, L.aligned, pf, L.cuts, m1, m2,
+      fa);
+  if (e != cudaSuccess) return fail("fused iteration launch", e);
   return 0;
 }
 
@@ -1027,6 +1169,14 @@ int32_t fdns_debug_trace(int32_t enable, uint64_t* out, int32_t n) {
     if (cudaMemcpyToSymbol(tiled::g_trace_n, &zero, sizeof(zero)) != cudaSuccess)
       return fail("trace log reset", cudaGetLastError());
   }
+  if (out && n > 0 && enable == 4) {   // fused-iteration timeline (debug)
+    const int m = std::min(n, tiled::TRACE_CTAS * tiled::FTRACE_W);
+    if (cudaMemcpyFromSymbol(out, tiled::g_ftrace, m * sizeof(uint64_t)) != cudaSuccess)
+      return fail("trace copy", cudaGetLastError());
+    on = 0;
+    cudaMemcpyToSymbol(tiled::g_trace_on, &on, sizeof(int));
+    return 0;
+  }
   if (out && n > 0 && enable == 3) {   // read the launch log: [count, records...]
     unsigned cnt = 0;
     if (cudaMemcpyFromSymbol(&cnt, tiled::g_trace_n, sizeof(cnt)) != cudaSuccess)
@@ -1150,6 +1300,38 @@ int32_t fdns_stage_planes(int32_t variant, const double* in, const double* saved
   if (with_fills)
     if (int e = launch_fills(variant, in, work, k, g, s)) return e;
   return launch_residual<1>(variant, in, saved, out, work, k, g, coef, wrap_mask, i_lo, i_hi, s);
+}
+
+int32_t fdns_iteration_sync_words(void) { return tiled::FUSED_SYNC_WORDS; }
+
+int32_t fdns_set_fused_iteration(int32_t enabled) {
+  const int32_t was = g_fused_iteration ? 1 : 0;
+  g_fused_iteration = enabled != 0;
+  return was;
+}
+
+int32_t fdns_iteration_supported(int32_t variant, int32_t wrap_mask, const fdns_problem* pb) {
+  if (validate(pb)) return 0;
+  return iteration_supported(variant, wrap_mask, make_geom(pb)) ? 1 : 0;
+}
+
+int32_t fdns_iteration(int32_t variant, double* X, double* Y, double* Z, uint32_t* sync,
+                       const double* coefs, int32_t wrap_mask, const fdns_problem* pb,
+                       void* stream) {
+  if (int e = validate(pb)) return e;
+  if (!X || !Y || !Z || !sync || !coefs) return fail("fdns_iteration: null pointer");
+  if (X == Y || Y == Z || X == Z) return fail("fdns_iteration needs three distinct bundles");
+  const Geom g = make_geom(pb);
+  if (!iteration_supported(variant, wrap_mask, g))
+    return fail("fdns_iteration: not supported for this variant/geometry (use fdns_stage)");
+  const Coef k = make_coef(pb);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int rc = variant == FDNS_SN
+                     ? launch_iteration_v<FDNS_SN>(X, Y, Z, sync, coefs, k, g, s)
+                     : launch_iteration_v<FDNS_RA>(X, Y, Z, sync, coefs, k, g, s);
+  if (rc) return rc;
+  count();
+  return check_launch("fused iteration kernel");
 }
 
 int32_t fdns_stage(int32_t variant, const double* in, const double* saved, double* out,

@@ -397,6 +397,61 @@ def kernel_path():
     yield lib
     lib.fdns_set_kernel_path(0)
     lib.fdns_set_tiled_grid(0)
+    lib.fdns_set_fused_iteration(0)
+
+
+def _run_fields(lib, variant, npts, cons, steps, fused, dt=1e-3):
+    lib.fdns_set_fused_iteration(int(fused))
+    g = grid_of(npts)
+    st = state_from_cons(g, cons)
+    ev = fd.ResidualEvaluator(g, C, variant)
+    assert ev.fused_iteration == (fused and variant in ("SN", "RA")
+                                  and npts[2] % 32 == 0 and npts[1] % 8 == 0
+                                  and not (variant == "SN" and npts[1] >= 96))
+    fd.run(st, fd.RKScheme(dt=dt), ev, steps)
+    torch.cuda.synchronize()
+    return st.bundle.cpu().numpy()
+
+
+@pytest.mark.parametrize("variant", ["SN", "RA"])
+@pytest.mark.parametrize("npts", [(5, 8, 32), (20, 16, 64), (64, 24, 96),
+                                  (128, 64, 64), (7, 64, 32)])
+def test_one_launch_iteration_equals_three_stages(kernel_path, variant, npts):
+    """fdns_iteration (the three stages in one cooperative launch, CTAs
+    waiting only on their stencil neighbourhood) is bitwise equal to three
+    fdns_stage launches -- whole padded bundles, ghosts included -- over
+    three RK3 steps, on geometries whose CTA ranges wrap planes, span tiles
+    or hold fewer planes than the stencil reach."""
+    F = npo.perturbed_taylor_green(max(npts), CO, 11)
+    cons = np.ascontiguousarray(
+        npo.interior(F[:5], 2)[:, :npts[0], :npts[1], :npts[2]])
+    want = _run_fields(kernel_path, variant, npts, cons, 3, False)
+    got = _run_fields(kernel_path, variant, npts, cons, 3, True)
+    assert np.array_equal(got, want)
+
+
+def test_one_launch_iteration_repeatable_and_counted(kernel_path):
+    """The fused 64^3 SN/RA iteration: one launch per RK3 step, and twenty
+    repeated 3-step runs (epochs advancing through the sync words) all
+    bitwise equal to the three-launch result (a missing neighbourhood wait
+    would show up as run-to-run differences)."""
+    n = 64
+    F = npo.taylor_green(n, CO)
+    cons = npo.interior(F[:5], 2)
+    for variant in ("SN", "RA"):
+        want = _run_fields(kernel_path, variant, (n,) * 3, cons, 3, False)
+        kernel_path.fdns_set_fused_iteration(1)
+        g = grid_of((n,) * 3)
+        ev = fd.ResidualEvaluator(g, C, variant)
+        assert ev.fused_iteration
+        for rep in range(20):
+            st = state_from_cons(g, cons)
+            c0 = kernel_path.fdns_launch_count()
+            fd.run(st, fd.RKScheme(dt=1e-3), ev, 3)
+            torch.cuda.synchronize()
+            # 3 iterations + the primitives before and after the loop
+            assert kernel_path.fdns_launch_count() - c0 == 3 + 2
+            assert np.array_equal(st.bundle.cpu().numpy(), want), (variant, rep)
 
 
 @pytest.mark.parametrize("variant,path", [(v, 0) for v in VARIANTS] + [("SN", 5)])
