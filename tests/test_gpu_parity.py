@@ -565,6 +565,94 @@ def test_slab_decomposition_bitwise_invariant(kernel_path, variant, nranks, spli
     assert np.array_equal(got, want)
 
 
+def _emulated_slab_run(variant, X0, npts, nranks, steps, dt, split=True):
+    """Run `steps` RK3 iterations of the device state bundle X0 (10 padded
+    fields, consistent ghosts) as `nranks` emulated z-slab ranks on one GPU
+    (host-sequenced: every rank's stage launches, then the plane copies of
+    Slab.exchange; no kernel waits on another).  Returns the interior
+    conservative fields gathered along axis 0, on the device."""
+    h = 2
+    slabs = [fd.Slab.partition(npts[0], r, nranks) for r in range(nranks)]
+    states, evs = [], []
+    for sl in slabs:
+        g = fd.make_grid(npts, (TWO_PI,) * 3, slab=sl)
+        st = fd.ConservativeState(g)
+        lo = sl.offset0
+        st.bundle[:5].copy_(X0[:5, lo:lo + sl.local_n0 + 2 * h])
+        fd.eval_primitives_fused(st, C)
+        states.append(st)
+        evs.append(fd.ResidualEvaluator(g, C, variant))
+
+    def exchange(bundles):
+        for r, sl in enumerate(slabs):
+            dn = slabs[r - 1]
+            b, bd, bu = bundles[r], bundles[r - 1], bundles[(r + 1) % nranks]
+            n = sl.local_n0
+            b[:, 0:h].copy_(bd[:, dn.local_n0:dn.local_n0 + h])
+            b[:, n + h:n + 2 * h].copy_(bu[:, h:2 * h])
+
+    scheme = fd.RKScheme(dt=dt)
+    for _ in range(steps):
+        X = [st.bundle for st in states]
+        YZ = [ev.workspace() for ev in evs]
+        src = [X, [y for y, _ in YZ], [z for _, z in YZ]]
+        dst = [src[1], src[2], X]
+        for k in range(3):
+            coef = scheme.alpha[k] * scheme.dt
+            if split:
+                for r in range(nranks):
+                    evs[r].stage_boundary(src[k][r], X[r], dst[k][r], coef)
+                exchange(dst[k])
+                for r in range(nranks):
+                    evs[r].stage_interior(src[k][r], X[r], dst[k][r], coef)
+            else:
+                for r in range(nranks):
+                    evs[r].stage(src[k][r], X[r], dst[k][r], coef)
+                exchange(dst[k])
+    out = torch.cat([st.bundle[:5, h:h + sl.local_n0, h:-h, h:-h]
+                     for st, sl in zip(states, slabs)], dim=1)
+    del states, evs
+    return out
+
+
+@pytest.mark.parametrize("variant", ["RA", "SS"])
+@pytest.mark.parametrize("nranks,split", [(2, False), (4, True), (8, True)])
+def test_c4_256_slab_decomposition_bitwise(variant, nranks, split):
+    """Config C4 (TGV 256^3, dt=8.5e-4, RA and SS, z-slabs over 1/2/4/8
+    GPUs: 256/128/64/32 planes per rank): two RK3 steps on 2, 4 and 8
+    emulated ranks, with the overlapped boundary/interior order, equal the
+    one-GPU fields bitwise (SURVEY 8e invariance gate)."""
+    n, dt = 256, 8.5e-4
+    g = grid_of((n,) * 3)
+    st = fd.taylor_green_init(g, C)
+    X0 = st.bundle.clone()
+    fd.run(st, fd.RKScheme(dt=dt), fd.ResidualEvaluator(g, C, variant), 2)
+    want = st.bundle[:5, 2:-2, 2:-2, 2:-2].clone()
+    del st
+    got = _emulated_slab_run(variant, X0, (n,) * 3, nranks, 2, dt, split)
+    assert torch.equal(got, want)
+
+
+def test_c5_512_slab_decomposition_bitwise():
+    """Config C5's multi-GPU layout on one GPU: TGV 512^3 (dt=4.2e-4) as 8
+    emulated z-slab ranks of 64 planes (SN on the 12-warp kernel, the
+    overlapped order), one RK3 step, bitwise equal to the one-GPU step --
+    with the 512^3 cross-variant test, the gate SURVEY 8d sets for sizes
+    without a CPU oracle."""
+    n, dt = 512, 4.2e-4
+    g = grid_of((n,) * 3)
+    st = fd.taylor_green_init(g, C)
+    X0 = st.bundle.clone()
+    fd.run(st, fd.RKScheme(dt=dt), fd.ResidualEvaluator(g, C, "SN"), 1)
+    want = st.bundle[:5, 2:-2, 2:-2, 2:-2].clone()
+    del st
+    torch.cuda.empty_cache()
+    got = _emulated_slab_run("SN", X0, (n,) * 3, 8, 1, dt, True)
+    assert torch.equal(got, want)
+    del X0, got, want
+    torch.cuda.empty_cache()
+
+
 # ------------------------------------------- bounds (compute-sanitizer is closed)
 @pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("npts", [(12, 16, 20), (9, 12, 7)])
