@@ -361,10 +361,14 @@ class ResidualEvaluator:
 
     @property
     def fused_iteration(self) -> bool:
-        """Whether a whole RK3 iteration runs as one launch here (SN on the
-        8-warp kernel / RA, one periodic GPU, grid tiled by 32x8 columns)."""
-        return bool(self.lib.fdns_iteration_supported(
-            self.plan.variant_id, self.wrap_mask, self.problem))
+        """Whether a whole RK3 iteration runs as one launch here (opt-in,
+        fdns_set_fused_iteration; SN on the 8-warp kernel / RA, one
+        periodic GPU, grid tiled by 32x8 columns).  Decided on first use:
+        set the library hooks before creating the evaluator."""
+        if getattr(self, "_fused_ok", None) is None:
+            self._fused_ok = bool(self.lib.fdns_iteration_supported(
+                self.plan.variant_id, self.wrap_mask, self.problem))
+        return self._fused_ok
 
     def iteration(self, X: torch.Tensor, Y: torch.Tensor, Z: torch.Tensor,
                   coefs) -> None:
