@@ -754,6 +754,24 @@ std::vector<int64_t> table_cuts(int64_t G, const TileCost& tc, int planes) {
 
 struct Launch { int64_t ctas; int aligned; const int64_t* cuts; };
 
+// Round-robin units (tiled::SPLIT_ROUNDS) for the SS/RS stage kernel: units
+// of ROUND_PLANES planes of one tile, dealt chunk-major, so neighbouring
+// tiles are staged at the same time and their shared halo columns (state
+// and the stored gradient boxes) hit in L2.  Measured whole RK3 steps at
+// 256^3: SS +6.4%, RS +1.8% with 64-plane units (32: +4.8% / 0%; 16:
+// slower); at 128^3 the extra ramps cost more than the L2 hits win (SS
+// -1.7%), and SN/RA (FP64-bound, far from the HBM roof) lose 5-9% at every
+// size, so only SS/RS from 256 planes use it.  FDNS_ROUNDS=C overrides the
+// unit (0 disables).
+constexpr int ROUND_PLANES = 64;
+const int g_rounds_env = std::getenv("FDNS_ROUNDS") ? std::atoi(std::getenv("FDNS_ROUNDS")) : -1;
+inline int rounds_planes(int variant, int nplanes) {
+  if (variant != FDNS_SS && variant != FDNS_RS) return 0;
+  const int c = g_rounds_env >= 0 ? g_rounds_env : ROUND_PLANES;
+  if (c <= 0 || nplanes % c != 0 || nplanes < 4 * c || g_tiled_ctas > 0) return 0;
+  return c;
+}
+
 Launch pick_launch(int ntk, int ntj, int planes, int wrap, int variant, cudaStream_t s,
                    bool allow_table = true, int ctas_per_sm = 1) {
   const int64_t tiles = (int64_t)ntk * ntj;
@@ -838,6 +856,21 @@ int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, 
   const int ntj = (g.n1 + tiled::TJ - 1) / tiled::TJ;
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
+  if constexpr (V == FDNS_SS || V == FDNS_RS) {
+    if (const int c = rounds_planes(V, nplanes)) {
+      static std::once_flag attr_rr;
+      std::call_once(attr_rr, [] {
+        cudaFuncSetAttribute(tiled::k_stage_tiled<V, MODE, LAZY, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      });
+      launch_pdl(tiled::k_stage_tiled<V, MODE, LAZY, false, true>,
+                 dim3((unsigned)std::min<int64_t>(num_sms(), total / c)), dim3(tiled::NT), smem,
+                 s, m, mg, ms, mp, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, c,
+                 (int)tiled::SPLIT_ROUNDS, pf, (const int64_t*)nullptr, m, m,
+                 tiled::FusedArgs{});
+      return 0;
+    }
+  }
   const Launch L = pick_launch(ntk, ntj, nplanes, wrap, V, s);
   launch_pdl(tiled::k_stage_tiled<V, MODE, LAZY>, dim3((unsigned)L.ctas), dim3(tiled::NT), smem, s,
              m, mg, ms, mp, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes,

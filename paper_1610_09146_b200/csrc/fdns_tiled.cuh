@@ -405,7 +405,7 @@ __device__ __forceinline__ void fill_slots(const Coef& k, const SAcc& a, double*
 // ring, prefetching across segment boundaries.
 // Partition modes of the (tile, plane) steps of one launch over G CTAs.
 enum SplitMode : int { SPLIT_CONTIGUOUS = 0, SPLIT_ALIGNED = 1, SPLIT_BALANCED = 2,
-                       SPLIT_TABLE = 3 };
+                       SPLIT_TABLE = 3, SPLIT_ROUNDS = 4 };
 // Ramp of a segment that starts inside a CTA's range (ring refill, five
 // planes converted, queues rebuilt), in quarter plane steps (measured
 // ~3.3 us vs ~3.0 us per step at 64^3).
@@ -413,10 +413,23 @@ constexpr int RAMP_MID_Q = 5;
 
 struct Segments {
   int64_t beg, end;   // [beg, end) in tile-major (tile * nplanes + plane) order
-  int n0;             // planes per tile in this launch
+  int n0;             // planes per tile (SPLIT_ROUNDS: per unit) in this launch
+  int64_t stride = 0; // SPLIT_ROUNDS: distance between this CTA's units (G * n0)
+  int64_t tiles = 1;  // SPLIT_ROUNDS: column tiles per plane chunk
   __host__ __device__ __forceinline__ int64_t seg_end(int64_t x) const {
     const int64_t tile_end = (x / n0 + 1) * (int64_t)n0;
     return tile_end < end ? tile_end : end;
+  }
+  // start of the segment after the one holding x (>= end: none)
+  __host__ __device__ __forceinline__ int64_t next(int64_t x) const {
+    return stride ? x - x % n0 + stride : seg_end(x);
+  }
+  // column tile and axis-0 plane (relative to the launch's first plane) of x
+  __host__ __device__ __forceinline__ int64_t tile_of(int64_t x) const {
+    return stride ? (x / n0) % tiles : x / n0;
+  }
+  __host__ __device__ __forceinline__ int plane_of(int64_t x) const {
+    return stride ? (int)((x / n0) / tiles * n0 + x % n0) : (int)(x % n0);
   }
   // CTA b of G over `total` = tiles * planes steps.
   //  SPLIT_ALIGNED (needs G >= tiles): each tile gets floor or ceil of
@@ -434,6 +447,18 @@ struct Segments {
                                                                 int mode,
                                                                 const int64_t* cuts = nullptr) {
     if (mode == SPLIT_TABLE) return Segments{cuts[b], cuts[b + 1], planes};
+    if (mode == SPLIT_ROUNDS) {
+      // units of `planes` consecutive planes of one tile, chunk-major
+      // (unit u = chunk * tiles + tile), dealt round-robin: in every round
+      // the G CTAs work on G consecutive units -- neighbouring tiles of the
+      // same plane chunk at the same time, so the halo columns one CTA's
+      // boxes read were just staged by its neighbours and hit in L2.
+      // The caller sets `tiles` (column tiles per plane chunk).
+      Segments r{b * (int64_t)planes, total, planes};
+      r.stride = G * (int64_t)planes;
+      if (r.beg > total) r.beg = total;
+      return r;
+    }
     const int64_t tiles = total / planes;
     if (mode == SPLIT_ALIGNED && G >= tiles) {
       const int64_t base = G / tiles, rem = G % tiles;
@@ -534,7 +559,7 @@ __device__ __forceinline__ void fused_retire(unsigned* sync) {
 #define FDNS_EARLY_GV 1
 #endif
 
-template <int V, int MODE, bool LAZY = true, bool FUSED = false>
+template <int V, int MODE, bool LAZY = true, bool FUSED = false, bool RR = false>
 __global__ void __launch_bounds__(NT, 1)
     k_stage_tiled(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tgw,
                   const __grid_constant__ CUtensorMap tsv, const __grid_constant__ CUtensorMap tgp,
@@ -556,6 +581,20 @@ __global__ void __launch_bounds__(NT, 1)
   const int tid = threadIdx.x;
   const int tk = tid % TK, tj = tid / TK;
   Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes, split, cuts);
+  if constexpr (RR) S.tiles = (int64_t)ntk * ((g.n1 + TJ - 1) / TJ);
+  // segment walk: contiguous tile-major ranges, or (RR) round-robin units
+  auto seg_next = [&](int64_t x) -> int64_t {
+    if constexpr (RR) return S.next(x);
+    else return S.seg_end(x);
+  };
+  auto tile_at = [&](int64_t x) -> int64_t {
+    if constexpr (RR) return S.tile_of(x);
+    else return x / nplanes;
+  };
+  auto plane_at = [&](int64_t x) -> int {
+    if constexpr (RR) return S.plane_of(x);
+    else return (int)(x % nplanes);
+  };
   if (S.beg >= S.end) {
     if constexpr (FUSED) {
       asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -599,7 +638,7 @@ __global__ void __launch_bounds__(NT, 1)
     issue_gb_tile(gs, (int)(tile % ntk) * TK, (int)(tile / ntk) * TJ, plane);
   };
   if constexpr (kGB) {
-    if (tid == 0) issue_gb(0, S.beg / nplanes, i_lo + (int)(S.beg % nplanes));
+    if (tid == 0) issue_gb(0, tile_at(S.beg), i_lo + plane_at(S.beg));
   }
   int gs = 0;   // step counter of this CTA (gradient-box parity)
 
@@ -612,11 +651,11 @@ __global__ void __launch_bounds__(NT, 1)
   int issued = 0;
   int p_len = 0, p_c0 = 0, p_c1 = 0, p_plane = 0, p_slot = 0;
   auto enter_segment = [&]() {
-    const int64_t tile = p_seg / nplanes;
+    const int64_t tile = tile_at(p_seg);
     p_len = (int)(S.seg_end(p_seg) - p_seg) + 4;
     p_c0 = (int)(tile % ntk) * TK + g.h - 2;
     p_c1 = (int)(tile / ntk) * TJ + g.h - 2;
-    p_plane = i_lo + (int)(p_seg % nplanes) - 2 + g.h;
+    p_plane = i_lo + plane_at(p_seg) - 2 + g.h;
   };
   if (tid == 0) enter_segment();
   auto issue_next = [&]() {
@@ -634,12 +673,12 @@ __global__ void __launch_bounds__(NT, 1)
     p_slot = p_slot + 1 == NR ? 0 : p_slot + 1;
     if (++p_r == p_len) {
       p_r = 0;
-      p_seg = S.seg_end(p_seg);
+      p_seg = seg_next(p_seg);
       if (p_seg < S.end) enter_segment();
     }
   };
   int stage_pos = 0;   // stream positions of one stage (steps + 4 per segment)
-  for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) stage_pos += (int)(S.seg_end(x) - x) + 4;
+  for (int64_t x = S.beg; x < S.end; x = seg_next(x)) stage_pos += (int)(S.seg_end(x) - x) + 4;
   int total_pos = stage_pos;   // issue limit: end of the current stage
   if (tid == 0)
     while (issued < total_pos && issued < NR) issue_next();
@@ -686,15 +725,15 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
   }
-  for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) {
+  for (int64_t x = S.beg; x < S.end; x = seg_next(x)) {
     const int64_t se = S.seg_end(x);
-    const int64_t tile = x / nplanes;
+    const int64_t tile = tile_at(x);
     const int k0 = (int)(tile % ntk) * TK, j0 = (int)(tile / ntk) * TJ;
     const int jj = j0 + tj, kk = k0 + tk;
     const bool active = jj < g.n1 && kk < g.n2;
     const int toff = (tj + 2) * PK + (tk + 2);
     const int nsteps = (int)(se - x);
-    const int i_seg = i_lo + (int)(x % nplanes);   // axis-0 index of step 0
+    const int i_seg = i_lo + plane_at(x);   // axis-0 index of step 0
     double q1[5], q2[5];   // SN axis-0 queues
     for (int t = 0; t < nsteps; ++t, ++w, ++gs, wsl = (wsl + 1 == NR ? 0 : wsl + 1)) {
       if (t == 0 && w > 0) {
@@ -799,8 +838,8 @@ __global__ void __launch_bounds__(NT, 1)
         if constexpr (kGB) {   // next step's centre gradient box
           if (t + 1 < nsteps) {
             issue_gb_tile(gs + 1, k0, j0, i_seg + t + 1);
-          } else if (se < S.end) {
-            issue_gb(gs + 1, se / nplanes, i_lo + (int)(se % nplanes));
+          } else if (seg_next(x) < S.end) {
+            issue_gb(gs + 1, tile_at(seg_next(x)), i_lo + plane_at(seg_next(x)));
           }
         }
       }
