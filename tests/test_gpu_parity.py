@@ -718,12 +718,14 @@ def test_c4_256_steps_match_c_oracle(variant):
 
 
 @pytest.mark.parametrize("variant", ["BL", "RA", "RS", "SN", "SS"])
-@pytest.mark.parametrize("npts", [(37, 45, 70), (130, 20, 132), (16, 130, 40)])
+@pytest.mark.parametrize("npts", [(37, 45, 70), (130, 20, 132), (16, 130, 40),
+                                  (256, 20, 44)])
 def test_ragged_grids_match_c_oracle(variant, npts):
     """Non-cubic grids whose extents are not multiples of the 32x8 tile
     (partial edge tiles, odd plane counts, n2 >= 128 with the sector-aligned
-    point-kernel map, a 1-tile-wide row): three RK3 steps of a perturbed TGV
-    state bitwise equal to the C oracle."""
+    point-kernel map, a 1-tile-wide row; 256 planes: SS/RS on the
+    round-robin unit split over ragged tiles): three RK3 steps of a
+    perturbed TGV state bitwise equal to the C oracle."""
     F = npo.manufactured(npts, CO)
     G = F.copy()
     c_oracle.run(G, CO, 1e-3, 3)
