@@ -1,24 +1,30 @@
 """Benchmark: grid-point x RK-stage updates/s per variant (BL/RA/SN/SS), fp64.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--n 64]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--grid 512]
                     [--variants BL,RA,SN,SS] [--impl ours|reference]
+                    [--scaling strong|weak]
 
-Workload (BASELINE.json configs[1]): Taylor-Green vortex 64^3, fp64,
-dt=3.385e-3, RK3 steps of each variant on one GPU.  A "step" is one full
-RK3 iteration (3 stages); the unit of work is one interior grid point
-advanced through one RK stage, so value = N^3 * 3 * K / seconds.
+Workload (BASELINE.json configs[4], "C5"): Taylor-Green vortex 512^3, fp64,
+dt=4.2e-4, RK3 steps of each of BL/RA/SN/SS -- the largest configuration
+that fits one GPU (BL's 90 padded fields are ~99 GB of the 180 GB HBM).  A
+"step" is one full RK3 iteration (3 stages); the unit of work is one
+interior grid point advanced through one RK stage, so value = N^3 * 3 * K /
+seconds.  Inputs are larger than L2 (one field is 1.1 GB) and L2 is flushed
+between timed steps anyway.
 
 Timing: W untimed warm-up steps, then K steps, each timed with CUDA events
-on the launching stream (the step is one captured CUDA graph); between
-timed steps L2 is flushed by writing a 256 MiB buffer (outside the events).
-Multi-GPU (torchrun): z-slab decomposition with NCCL halo exchange; the
-per-rank time is reduced with MAX; --scaling weak (default: each rank owns
-n planes, the grid is refined along axis 0) or strong (the n^3 grid split).
+on the launching stream (on one GPU the step is one captured CUDA graph).
+Multi-GPU: `--gpus N` without a launcher re-executes this script under
+`torch.distributed.run` with N ranks (127.0.0.1); each rank owns a z-slab
+(axis 0) of the grid, the periodic 2-plane halo exchange runs over NCCL,
+overlapped with the interior planes, and the per-rank time is reduced with
+MAX.  --scaling strong (default: the n^3 grid split over N ranks, the
+north-star's 8-GPU 512^3 target) or weak (each rank owns n planes).
 
 --impl reference times the reference algorithm's CPU restatement (the C +
-OpenMP oracle, pinned bitwise to the reference) on the host cores; the
-reference package itself is pure Python/numba and does not exist on the GPU
-box.
+OpenMP oracle, pinned bitwise to the reference) on the host cores, on the
+same workload and config; the reference package itself is pure
+Python/numba and does not exist on the GPU box.
 """
 
 from __future__ import annotations
@@ -39,7 +45,10 @@ sys.path.insert(0, ROOT)
 METRIC = ("grid-pt·RK-stage updates/s per variant (BL/RA/SN/SS), fp64; "
           "% of roofline")
 UNIT = "grid-pt*RK-stage/s"
-DT = {64: 3.385e-3, 128: 1.69e-3, 256: 8.5e-4, 512: 4.2e-4, 32: 2e-3}
+DT = {64: 3.385e-3, 128: 1.69e-3, 256: 8.5e-4, 512: 4.2e-4, 32: 2e-3,
+      1024: 2.1e-4}
+CONFIG_NAMES = {32: "C1", 64: "C2", 128: "C3", 256: "C4", 512: "C5",
+                1024: "C5 (weak counterpart)"}
 
 # Algorithmic per-point costs of one fused stage kernel:
 #   flops F_v = residual source flops + 10 (update) + 13 (primitives)
@@ -115,11 +124,15 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ setup
-def init_dist():
+def init_dist(args):
+    """Rank/world from the launcher's environment; NCCL for N > 1.  A world
+    size that disagrees with --gpus is an error, not a silent 1-GPU run."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1 and args.impl == "ours":
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -127,8 +140,55 @@ def init_dist():
     return rank, world, local
 
 
+def launcher_cmd(argv, gpus: int, port: int) -> list:
+    """The torchrun command that runs this script on `gpus` ranks of one
+    node (127.0.0.1 rendezvous), forwarding the original arguments."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={gpus}", "--master-addr=127.0.0.1",
+            f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def self_launch(args, argv) -> int | None:
+    """`--gpus N` (N > 1) with no launcher around us: re-execute under
+    torch.distributed.run with N ranks and return its exit code."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    return subprocess.call(launcher_cmd(argv, args.gpus, port))
+
+
 def cpu_cores() -> int:
     return len(os.sched_getaffinity(0))
+
+
+def global_grid(args, world: int) -> tuple:
+    """Global grid points: n^3, or (n*world, n, n) for weak scaling."""
+    n = args.n
+    if world > 1 and args.scaling == "weak":
+        return (n * world, n, n)
+    return (n, n, n)
+
+
+def config_dict(args, world: int) -> dict:
+    """The workload description both arms print (identical by construction)."""
+    npts = global_grid(args, world)
+    n = args.n
+    name = CONFIG_NAMES.get(n, "custom")
+    weak = npts[0] != n
+    return {"workload": f"{name}: TGV {'x'.join(map(str, npts))} fp64, "
+                        f"dt={DT.get(n)}, RK3 steps, variants "
+                        + "/".join(args.variants)
+                        + (f", z-slab over {world} GPUs ({args.scaling} "
+                           "scaling)" if world > 1 else ""),
+            "grid": list(npts), "dt": DT.get(n),
+            "variants": list(args.variants),
+            "parallelism": f"z-slab x{world}" + (" (weak)" if weak else ""),
+            "l2": "inputs larger than L2 (1.1 GB per 512^3 field); L2 also "
+                  "flushed between timed steps (256 MiB write)"}
 
 
 def run_cpu_oracle(npts, steps: int, warmup: int = 1, min_seconds: float = 0.0):
@@ -142,24 +202,34 @@ def run_cpu_oracle(npts, steps: int, warmup: int = 1, min_seconds: float = 0.0):
     npts = (npts,) * 3 if isinstance(npts, int) else tuple(npts)
     n = npts[1]
     F = npo.taylor_green(n, c) if len(set(npts)) == 1 else npo.manufactured(npts, c)
-    c_oracle.run(F, c, DT.get(n, 3.385e-3), warmup)
+    # every host thread, explicitly: torchrun exports OMP_NUM_THREADS=1
+    threads = cpu_cores()
+    if warmup:
+        c_oracle.run(F, c, DT.get(n, 3.385e-3), warmup, nthreads=threads)
     done, dt = 0, 0.0
     while done == 0 or dt < min_seconds:
         t0 = time.perf_counter()
-        c_oracle.run(F, c, DT.get(n, 3.385e-3), steps)
+        c_oracle.run(F, c, DT.get(n, 3.385e-3), steps, nthreads=threads)
         dt += time.perf_counter() - t0
         done += steps
     return float(np.prod(npts)) * 3 * done / dt, dt, done
 
 
 # ------------------------------------------------------------------ ours
-def bench_variant(fd, variant, grid, steps, warmup, flush_buf, lib, clocks=None,
-                  clock_window=0.0):
+def fresh_state(fd, grid, cons_host):
+    """A device state from the cached host TGV arrays (same bits as
+    taylor_green_init; the 512^3 host evaluation runs once per process)."""
+    from paper_1610_09146_b200.diagnostics import state_from_conservative
+    return state_from_conservative(grid, fd.PhysicalConstants(), cons_host)
+
+
+def bench_variant(fd, variant, grid, cons_host, steps, warmup, flush_buf, lib,
+                  clocks=None, clock_window=0.0):
     import torch
     from paper_1610_09146_b200 import _lib
     from paper_1610_09146_b200.timeloop import IterationState, _fused_iteration
     c = fd.PhysicalConstants()
-    state = fd.taylor_green_init(grid, c)
+    state = fresh_state(fd, grid, cons_host)
     ev = fd.ResidualEvaluator(grid, c, variant)
     scheme = fd.RKScheme(dt=DT.get(grid.npoints[1], 3.385e-3))
     it = IterationState(state, saved=False)
@@ -190,17 +260,15 @@ def bench_variant(fd, variant, grid, steps, warmup, flush_buf, lib, clocks=None,
     stream = torch.cuda.current_stream()
     if clock_window > 0:
         # untimed replay of the same step, long enough for nvidia-smi to
-        # sample the clocks under exactly this load (the timed K steps below
-        # last only milliseconds)
+        # sample the clocks under exactly this load
         with clocks:
             t_end = time.perf_counter() + clock_window
             while time.perf_counter() < t_end:
-                for _ in range(20):
+                for _ in range(4):
                     step()
                 torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True),
             torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    n_launch0 = lib.fdns_launch_count()
     launches_per_step = None
     if graph is not None:
         # graph replays do not pass through the ABI counter: count one
@@ -227,20 +295,24 @@ def bench_variant(fd, variant, grid, steps, warmup, flush_buf, lib, clocks=None,
                 else lib.fdns_launch_count() - n_launch0)
 
     # informational: one stage (all its launches) timed alone after an L2
-    # flush, eager launch
+    # flush, eager launch, with a saved state distinct from the input
     X = state.bundle
     Y, Z = ev.workspace()
     kev = [(torch.cuda.Event(enable_timing=True),
-            torch.cuda.Event(enable_timing=True)) for _ in range(6)]
+            torch.cuda.Event(enable_timing=True)) for _ in range(5)]
     for a, b in kev:
         _lib.check(lib.fdns_l2_flush(_lib.ptr(flush_buf), flush_buf.numel(),
                                      _lib.stream_handle()), "flush")
         a.record(stream)
-        ev.stage(Y, X, Z, 1e-30)   # same work as a real stage
+        if multi:
+            ev.stage_exchanged(Y, X, Z, 1e-30)
+        else:
+            ev.stage(Y, X, Z, 1e-30)   # a stage-1/2 workload
         b.record(stream)
     torch.cuda.synchronize()
     stage_ms = float(np.median([a.elapsed_time(b) for a, b in kev]))
-    del graph
+    del graph, state, ev, it, X, Y, Z
+    torch.cuda.empty_cache()
     return total_ms, launches, stage_ms
 
 
@@ -273,6 +345,7 @@ def stage_sweep(fd, lib, sizes, variants, flush, fp64_tf, hbm_peak):
         for v in variants:
             ev = fd.ResidualEvaluator(g, c, v)
             Y, Z = ev.workspace()
+            Y.copy_(s.bundle)
             ts = []
             for r in range(5):
                 _lib.check(lib.fdns_l2_flush(_lib.ptr(flush), flush.numel(),
@@ -280,7 +353,7 @@ def stage_sweep(fd, lib, sizes, variants, flush, fp64_tf, hbm_peak):
                 a = torch.cuda.Event(enable_timing=True)
                 b = torch.cuda.Event(enable_timing=True)
                 a.record()
-                ev.stage(s.bundle, s.bundle, Y, 1e-30)
+                ev.stage(Y, s.bundle, Z, 1e-30)   # saved != input
                 b.record()
                 torch.cuda.synchronize()
                 if r >= 2:
@@ -325,7 +398,7 @@ def fp64_peak(lib):
 E2E_CHUNKS = 5
 
 
-def bench_e2e(fd, variant, grid, steps):
+def bench_e2e(fd, variant, grid, cons_host, steps):
     """Same metric through the public API with host buffers: per step the
     five conservative fields (padded, as the reference holds them) are
     uploaded from pinned memory, one fused RK3 iteration runs, and the new
@@ -335,7 +408,7 @@ def bench_e2e(fd, variant, grid, steps):
     import torch
     from paper_1610_09146_b200.hostio import HostStepper
     c = fd.PhysicalConstants()
-    state = fd.taylor_green_init(grid, c)
+    state = fresh_state(fd, grid, cons_host)
     ev = fd.ResidualEvaluator(grid, c, variant)
     scheme = fd.RKScheme(dt=DT.get(grid.npoints[1], 3.385e-3))
     host = HostStepper.pinned_buffers(grid)
@@ -345,6 +418,10 @@ def bench_e2e(fd, variant, grid, steps):
         stepper.step()
     stepper.wait()
     torch.cuda.synchronize()
+    multi = grid.slab is not None and grid.slab.nranks > 1
+    if multi:
+        import torch.distributed as dist
+        dist.barrier()
     stream = torch.cuda.current_stream()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
@@ -354,28 +431,69 @@ def bench_e2e(fd, variant, grid, steps):
     b.record(stream)
     torch.cuda.synchronize()
     sec = a.elapsed_time(b) / 1e3
-    if grid.slab is not None and grid.slab.nranks > 1:
-        import torch.distributed as dist
+    if multi:
         t = torch.tensor([sec], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         sec = float(t[0])
     npts = float(np.prod(grid.npoints))
     nbytes = host.numel() * 8
+    stepper.close() if hasattr(stepper, "close") else None
+    del stepper, state, ev, host
+    torch.cuda.empty_cache()
     return {"value": npts * 3 * steps / sec, "unit": UNIT,
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-            "variant": variant,
+            "steps": steps, "variant": variant,
             "path": "hostio.HostStepper: pinned host fields -> advance one "
                     "RK3 iteration -> host; field copies in chunks, each "
                     "upload chunk right behind the previous result's "
-                    f"download of it ({E2E_CHUNKS} chunks/field), CUDA graphs"}
+                    f"download of it ({E2E_CHUNKS} chunks/field), CUDA graphs"
+                    + ("; per rank: its slab" if multi else "")}
+
+
+def variant_roofline(v, rec, fp64_tf, hbm_peak, hbm_src, n):
+    """The roofline object of one variant's stage: algorithmic
+    flops or bytes per point x points / average stage duration, against the
+    in-run FP64 issue probe or the measured HBM copy bandwidth; plus the
+    executed-FP64 view where ncu counted the stage kernel's FP64
+    instructions."""
+    if rec["bound"] == "fp64":
+        roof = {"bound": "fp64", "achieved": rec["achieved_tflops"],
+                "peak": fp64_tf, "unit": "TFLOP/s",
+                "peak_source": "measured in-run (DADD issue probe, no-FMA)"}
+    else:
+        roof = {"bound": "hbm", "achieved": rec["achieved_gbs"],
+                "peak": hbm_peak, "unit": "GB/s",
+                "peak_source": f"{hbm_src} (MEASURED_PEAKS.json hbm_gbs)"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    tr = measured_traffic(v, n)
+    roof["traffic"] = tr["bytes_per_launch"] if tr else None
+    roof["traffic_detail"] = tr
+    ex = (tr or {}).get("fp64_insts_per_point")
+    if ex:
+        pts_per_s = rec["local_pts"] / (rec["stage_kernel_ms"] / 1e3)
+        roof["executed_fp64_view"] = {
+            "fp64_insts_per_point": ex,
+            "frac_of_fp64_issue_peak": pts_per_s * ex / (fp64_tf * 1e12),
+            "source": tr["source"]}
+    roof["kernel"] = (f"RK stage ({v}): " + {
+        "SN": "fused stage kernel (residual + RK update + primitives)",
+        "RA": "fused stage kernel (residual + RK update + primitives)",
+        "SS": "9-gradient fill + fused stage kernel",
+        "RS": "9-gradient fill + fused stage kernel",
+        "BL": "60-array fills + residual/update kernel"}[v])
+    roof["duration"] = ("average stage duration over the timed region = "
+                        "timed steps / (3 x steps); L2 flushed before every "
+                        "step")
+    return roof
 
 
 def main_ours(args):
     import torch
-    rank, world, local = init_dist()
+    rank, world, local = init_dist(args)
     torch.cuda.set_device(local)
     import paper_1610_09146_b200 as fd
     from paper_1610_09146_b200 import _lib
+    from paper_1610_09146_b200.diagnostics import taylor_green_conservative
     lib = _lib.load()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -383,101 +501,78 @@ def main_ours(args):
     hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
 
     n = args.n
-    slab = None
-    if world > 1:
-        n0 = n * world if args.scaling == "weak" else n
-        slab = fd.Slab.from_process_group(n0)
-        grid = fd.make_grid((n0, n, n), (2 * np.pi,) * 3, slab=slab)
-    else:
-        grid = fd.make_grid((n, n, n), (2 * np.pi,) * 3)
+    npts = global_grid(args, world)
+    slab = fd.Slab.from_process_group(npts[0]) if world > 1 else None
+    grid = fd.make_grid(npts, (2 * np.pi,) * 3, slab=slab)
     npts_total = float(np.prod(grid.npoints))
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        comm = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                "local_planes": grid.local_npoints[0]}
+    t0 = time.perf_counter()
+    cons_host = taylor_green_conservative(grid, fd.PhysicalConstants())
+    init_s = time.perf_counter() - t0
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     fp64_tf = fp64_peak(lib)
     results = {}
     clocks = ClockSampler(local, period_ms=20)
-    if True:
-        for v in args.variants:
-            total_ms, launches, cold_ms = bench_variant(
-                fd, v, grid, args.steps, args.warmup, flush, lib, clocks,
-                args.clock_window)
-            if world > 1:
-                import torch.distributed as dist
-                t = torch.tensor([total_ms, cold_ms], device="cuda")
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                total_ms, cold_ms = t.tolist()
-            # average duration of one RK stage over the timed region: the
-            # step is exactly three stages' launches back to back in one
-            # CUDA graph (for SN: three launches of the fused stage kernel)
-            stage_ms = total_ms / (3 * args.steps)
-            local_pts = float(np.prod(grid.local_npoints))
-            val = npts_total * 3 * args.steps / (total_ms / 1e3)
-            flops = STAGE_FLOPS[v] * local_pts / (stage_ms / 1e3) / 1e12
-            gbs = stage_bytes(v) * local_pts / (stage_ms / 1e3) / 1e9
-            t_fp64 = STAGE_FLOPS[v] / (fp64_tf * 1e12)
-            t_hbm = stage_bytes(v) / (hbm_peak * 1e9)
-            bound = "fp64" if t_fp64 >= t_hbm else "hbm"
-            results[v] = {
-                "value": val, "ms_per_step": total_ms / args.steps,
-                "gpu_launches": launches,
-                "stage_kernel_ms": stage_ms,
-                "stage_kernel_ms_isolated_cold": cold_ms,
-                "stage_kernel_flops_per_pt": STAGE_FLOPS[v],
-                "stage_kernel_bytes_per_pt": stage_bytes(v),
-                "achieved_tflops": flops, "achieved_gbs": gbs,
-                "bound": bound,
-                "roofline_pt_stage_per_s": 1.0 / max(t_fp64, t_hbm),
-                "frac_of_roofline": (local_pts / (stage_ms / 1e3))
-                * max(t_fp64, t_hbm),
-            }
+    for v in args.variants:
+        total_ms, launches, cold_ms = bench_variant(
+            fd, v, grid, cons_host, args.steps, args.warmup, flush, lib,
+            clocks, args.clock_window)
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([total_ms, cold_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total_ms, cold_ms = t.tolist()
+        # average duration of one RK stage over the timed region: the step
+        # is exactly three stages' launches back to back
+        stage_ms = total_ms / (3 * args.steps)
+        local_pts = float(np.prod(grid.local_npoints))
+        val = npts_total * 3 * args.steps / (total_ms / 1e3)
+        flops = STAGE_FLOPS[v] * local_pts / (stage_ms / 1e3) / 1e12
+        gbs = stage_bytes(v) * local_pts / (stage_ms / 1e3) / 1e9
+        t_fp64 = STAGE_FLOPS[v] / (fp64_tf * 1e12)
+        t_hbm = stage_bytes(v) / (hbm_peak * 1e9)
+        bound = "fp64" if t_fp64 >= t_hbm else "hbm"
+        rec = {
+            "value": val, "ms_per_step": total_ms / args.steps,
+            "gpu_launches": launches,
+            "stage_kernel_ms": stage_ms,
+            "stage_ms_isolated_cold": cold_ms,
+            "stage_flops_per_pt": STAGE_FLOPS[v],
+            "stage_bytes_per_pt": stage_bytes(v),
+            "achieved_tflops": flops, "achieved_gbs": gbs,
+            "bound": bound, "local_pts": local_pts,
+            "roofline_pt_stage_per_s": 1.0 / max(t_fp64, t_hbm),
+        }
+        rec["roofline"] = variant_roofline(v, rec, fp64_tf, hbm_peak,
+                                           hbm_src, n)
+        results[v] = rec
     head = max(results, key=lambda v: results[v]["value"])   # same on all ranks
     r = results[head]
     # end-to-end through the public API with host buffers (all ranks)
-    e2e = bench_e2e(fd, head, grid, max(3, min(args.steps, 20)))
+    e2e = bench_e2e(fd, head, grid, cons_host, max(3, min(args.steps,
+                                                          args.e2e_steps)))
     if rank != 0:
         return
-    if r["bound"] == "fp64":
-        roof = {"bound": "fp64", "achieved": r["achieved_tflops"],
-                "peak": fp64_tf, "unit": "TFLOP/s",
-                "peak_source": "measured in-run (DADD issue probe, no-FMA)"}
-    else:
-        roof = {"bound": "hbm", "achieved": r["achieved_gbs"],
-                "peak": hbm_peak, "unit": "GB/s",
-                "peak_source": f"{hbm_src} (MEASURED_PEAKS.json hbm_gbs)"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    # contract: `traffic` = dram read+write bytes per launch (a number, or
-    # null); where it comes from goes beside it
-    tr = measured_traffic(head, n)
-    roof["traffic"] = tr["bytes_per_launch"] if tr else None
-    roof["traffic_detail"] = tr
-    # where the compiler's CSE executes fewer FP64 instructions
-    # than the source flops, the ceiling at the executed count is the
-    # stricter view (ncu: DADD + DMUL + DFMA thread instructions per point)
-    ex = (tr or {}).get("fp64_insts_per_point") if roof["bound"] == "fp64" else None
-    if ex:
-        pts_per_s = roof["achieved"] * 1e12 / STAGE_FLOPS[head]   # per stage launch
-        roof["executed_fp64_view"] = {
-            "fp64_insts_per_point": ex,
-            "frac": pts_per_s * ex / (roof["peak"] * 1e12),
-            "source": tr["source"]}
-    roof["kernel"] = f"fused stage ({head}): residual+RK update+primitives"
-    roof["duration"] = ("average stage launch duration over the timed "
-                        "region = timed steps / (3 x steps); L2 flushed "
-                        "before every step")
+    roof = dict(r["roofline"])
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        v, sec, done = run_cpu_oracle(n, max(1, args.cpu_steps),
+        v, sec, done = run_cpu_oracle(n, 1, warmup=args.cpu_warmup,
                                       min_seconds=args.cpu_seconds)
         cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
                "sample": f"C+OpenMP oracle (SN route, pinned bitwise to the "
-                         f"reference), TGV {n}^3, {done} RK3 steps after 1 "
-                         f"warm-up, {sec:.1f} s"}
+                         f"reference), TGV {n}^3, {done} RK3 steps after "
+                         f"{args.cpu_warmup} warm-up, {sec:.1f} s"}
     sizes = {}
     if world == 1 and args.sizes:
         sizes = stage_sweep(fd, lib, [int(x) for x in args.sizes.split(",")],
                             args.variants, flush, fp64_tf, hbm_peak)
-
 
     line = {
         "metric": METRIC, "value": r["value"], "unit": UNIT,
@@ -486,39 +581,38 @@ def main_ours(args):
         "scaling": args.scaling if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: analytic Taylor-Green vortex initial state "
-                "(BASELINE.json configs[1])",
-        "config": {"workload": f"TGV {n}^3 fp64, dt={DT.get(n)}, RK3 steps, "
-                               "variants " + "/".join(args.variants),
-                   "grid": list(grid.npoints), "headline_variant": head,
-                   "parallelism": f"z-slab x{world}",
-                   "l2": "flushed between timed steps (256 MiB write)"},
-        "variants": {v: {k: x for k, x in d.items()} for v, d in results.items()},
+                "(BASELINE.json configs[4]; host numpy, the reference's "
+                "expressions)",
+        "config": config_dict(args, world),
+        "headline_variant": head,
+        "variants": results,
         "roofline": roof,
         "fp64_peak_tflops_measured": fp64_tf,
         "cpu_baseline": cpu,
         "stage_sweep": sizes,
         "e2e": e2e,
         "gpu_launches": r["gpu_launches"],
+        "comm": comm,
+        "host_init_seconds": init_s,
         "clocks": {**clocks.summary(),
                    "window": f"{args.clock_window:.1f} s replay of each "
                              "variant's step right before its timed region"},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
 
 
 def main_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank, world, _ = init_dist(args)
     if rank != 0:
         return
-    n = args.n
-    # the same grid as our arm: weak scaling stacks one n^3 block per rank
-    npts = (n * world, n, n) if world > 1 and args.scaling == "weak" else (n, n, n)
-    # K "steps" as asked; the timed sample is at least --cpu-seconds of RK3
-    # iterations (one iteration of this grid is ~20 ms on 16 cores, so a
-    # handful would time mostly noise)
-    steps = max(1, min(args.steps, args.cpu_steps))
-    val, sec, iters = run_cpu_oracle(npts, steps, warmup=1,
+    npts = global_grid(args, world)
+    # each "step" is one RK3 iteration of the configured grid; the timed
+    # sample is at least --cpu-seconds of them (a 512^3 iteration is
+    # ~8-10 s on 16 cores, so the sample is a bounded number of iterations)
+    val, sec, iters = run_cpu_oracle(npts, 1, warmup=args.cpu_warmup,
                                      min_seconds=args.cpu_seconds)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
@@ -530,41 +624,51 @@ def main_reference(args):
         "data": "synthetic: analytic Taylor-Green vortex initial state"
                 if len(set(npts)) == 1 else
                 "synthetic: smooth manufactured state of the slab grid's shape",
-        "config": {"workload": f"TGV {n}^3 fp64, dt={DT.get(n)}, RK3 steps"
-                               + (f", x{world} ranks (weak)" if npts[0] != n else ""),
-                   "grid": list(npts)},
+        "config": config_dict(args, world),
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cpu_cores(),
                          "kind": "port",
                          "sample": f"C+OpenMP restatement of the reference "
-                                   f"(SN route), grid {npts}, {iters} RK3 "
-                                   f"iterations after 1 warm-up, {sec:.1f} s"},
+                                   f"(SN route), grid {list(npts)}, {iters} "
+                                   f"RK3 iterations after {args.cpu_warmup} "
+                                   f"warm-up, {sec:.1f} s, rank 0 only"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
 
 
-def main():
+def parse_args(argv):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--n", type=int, default=64)
+    ap.add_argument("--grid", dest="n", type=int, default=512,
+                    help="cube edge n (the workload is TGV n^3)")
     ap.add_argument("--variants", default="BL,RA,SN,SS")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--cpu-steps", type=int, default=20)
-    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="minimum timed CPU work for the baseline sample")
+    ap.add_argument("--cpu-warmup", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--clock-window", type=float, default=0.5,
                     help="seconds of untimed step replay sampled for clocks")
-    ap.add_argument("--sizes", default="128,256",
-                    help="extra grid sizes for the steady-state stage sweep")
+    ap.add_argument("--sizes", default="",
+                    help="extra grid sizes for a single-stage sweep")
     ap.add_argument("--no-cpu", action="store_true")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     args.variants = [v.strip().upper() for v in args.variants.split(",")]
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    return args
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse_args(argv)
+    rc = self_launch(args, argv)
+    if rc is not None:
+        sys.exit(rc)
     if args.impl == "reference":
         main_reference(args)
     else:

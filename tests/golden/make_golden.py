@@ -103,7 +103,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true",
                     help="also run the 64^3/100-step and 128^3/200-step cases")
+    ap.add_argument("--large", action="store_true",
+                    help="only the C4 (256^3, 100 steps) and C5 (512^3, 2 "
+                         "steps) runs, merged into golden_meta.json")
     args = ap.parse_args()
+    if args.large:
+        return main_large()
     meta = {"generator": "tests/golden/make_golden.py",
             "reference": "/root/reference/pkg (fdns 0.1.0)",
             "perturb_seed": PERTURB_SEED}
@@ -178,6 +183,36 @@ def main():
     prev.update(meta)
     path.write_text(json.dumps(prev, indent=1) + "\n")
     print("wrote", sorted(arrays), sorted(meta))
+
+
+def main_large():
+    """Configs C4 and C5 (BASELINE.json configs[3], configs[4]) through the
+    reference's SN route (all plans are bitwise equal in the reference,
+    `test_output.txt:247`): final-field SHA-256 plus the diagnostics
+    history.  C4: TGV 256^3, dt=8.5e-4, 100 steps (sampled every 10);
+    C5: TGV 512^3, dt=4.2e-4, 2 steps (sampled every step) -- the most this
+    container's 62 GB and the reference's single-threaded numpy stages
+    allow in reasonable time."""
+    meta = {}
+    g256 = cube(256)
+    st = taylor_green_init(g256, C)
+    meta["c4_tgv256"], _ = run_case(g256, st, "SN", 8.5e-4, 100, 10)
+    print("c4", meta["c4_tgv256"]["ref_seconds"], flush=True)
+    _merge(meta)
+    del st
+    g512 = cube(512)
+    st = taylor_green_init(g512, C)
+    meta = {}
+    meta["c5_tgv512"], _ = run_case(g512, st, "SN", 4.2e-4, 2, 1)
+    print("c5", meta["c5_tgv512"]["ref_seconds"], flush=True)
+    _merge(meta)
+
+
+def _merge(meta):
+    path = OUT / "golden_meta.json"
+    prev = json.loads(path.read_text()) if path.exists() else {}
+    prev.update(meta)
+    path.write_text(json.dumps(prev, indent=1) + "\n")
 
 
 if __name__ == "__main__":
