@@ -75,7 +75,9 @@ int32_t fdns_derivative(const double* f, double* out, int32_t op,
  * writes the interior of the 5 residual fields -- replaces
  * ResidualEvaluator.evaluate (plan.py:394-416) and the generated kernel
  * (codegen.py:156-179).  `work` holds fdns_workarray_count(variant) padded
- * fields (may be NULL when the count is 0). */
+ * fields (may be NULL when the count is 0).  `out`, `state` and `work` must
+ * not overlap (the kernels read the state's stencil while writing `out`);
+ * an overlapping call fails. */
 int32_t fdns_residual(int32_t variant, const double* state, double* work,
                       double* out, const fdns_problem* pb, void* stream);
 
@@ -96,30 +98,6 @@ int32_t fdns_stage(int32_t variant, const double* in, const double* saved,
                    double* out, double* work, double coef, int32_t wrap_mask,
                    const fdns_problem* pb, void* stream);
 
-/* One whole RK3 iteration (advance_iteration, timeloop.py:88-94) of a
- * periodic one-GPU state in ONE launch: stage 0 reads X and writes Y, stage 1
- * reads Y and writes Z, stage 2 reads Z and writes X in place (saved state X
- * throughout, so the save_state copy of timeloop.py:59-61 disappears);
- * coefs[k] = alpha[k]*dt.  Between stages every CTA waits only for the CTAs
- * that wrote its stencil neighbourhood (no grid-wide barrier, no launch
- * gap).  Bitwise equal to three fdns_stage calls.  `sync` is
- * fdns_iteration_sync_words() uint32 words, zeroed once by the caller and
- * reused by every later call on the same stream.  Supported for SN (8-warp
- * tiled kernel) and RA on grids tiled exactly by 32 x 8 columns with
- * wrap_mask 0b111 (fdns_iteration_supported); otherwise it fails and the
- * caller uses fdns_stage.  Disabled unless fdns_set_fused_iteration(1). */
-int32_t fdns_iteration(int32_t variant, double* X, double* Y, double* Z,
-                       uint32_t* sync, const double* coefs, int32_t wrap_mask,
-                       const fdns_problem* pb, void* stream);
-int32_t fdns_iteration_supported(int32_t variant, int32_t wrap_mask,
-                                 const fdns_problem* pb);
-int32_t fdns_iteration_sync_words(void);
-/* Enable or disable (default; FDNS_FUSED_ITERATION=1 enables) the one-launch
- * iteration; returns the previous setting.  Off by default because the
- * inter-stage memory-flag hand-off measured slower than three programmatic
- * (PDL) launches -- see DESIGN.md 3.4. */
-int32_t fdns_set_fused_iteration(int32_t enabled);
-
 /* The fused stage restricted to local axis-0 planes [i_lo, i_hi) (interior
  * indices); work-array fills over the whole slab first when with_fills.  A
  * z-slab rank updates its 2h boundary planes, starts the halo exchange on a
@@ -134,8 +112,7 @@ int32_t fdns_stage_planes(int32_t variant, const double* in,
 /* Test hook selecting the kernel family: 0 = default (TMA-staged tiled
  * kernels where the row pitch allows; SN on the 12-warp kernel where its
  * tile rows fit the grid), 1 = one-thread-per-point kernels (global-memory
- * taps) for every variant; SN only: 2 = the 8-warp tiled kernel, 3 = two
- * warp groups per point (experimental; slower on B200),
+ * taps) for every variant; SN only: 2 = the 8-warp tiled kernel,
  * 4 = eagerly evaluated derivatives, 5 = the 12-warp kernel.  All paths are
  * parity-tested. */
 void fdns_set_kernel_path(int32_t path);
@@ -149,6 +126,17 @@ void fdns_set_tiled_grid(int32_t ctas);
  * a stage's CTAs are dispatched as the previous stage's retire and wait in
  * griddepcontrol.wait before any global access. */
 void fdns_set_pdl(int32_t enabled);
+
+/* L2 prefetches issued by the stage kernels' producer thread (default: both
+ * on; env FDNS_NO_SAVED_PREFETCH / FDNS_NO_GRAD_PREFETCH turn them off at
+ * load): bit 0 = the saved state of RK stages 2/3, bit 1 = SS/RS's nine
+ * stored gradients.  A kill switch and an A/B hook. */
+void fdns_set_prefetch(int32_t mask);
+
+/* Test hook: unit size (planes) of the SS/RS round-robin split (-1 =
+ * default: 64-plane units from 256 planes; 0 = off; c > 0 = c-plane units
+ * wherever the plane count is a multiple of c and at least 4c). */
+void fdns_set_rounds(int32_t planes);
 
 /* Debug timeline of the tiled stage kernels: enable (1) / disable (0) the
  * per-CTA %globaltimer stamps (entry, prologue done, first window ready,

@@ -53,14 +53,11 @@ EXPORTS = {
                         ctypes.POINTER(Problem), _VP]),
     "fdns_stage_planes": (_I, [_I, _VP, _VP, _VP, _VP, ctypes.c_double, _I, _I,
                                _I, _I, ctypes.POINTER(Problem), _VP]),
-    "fdns_iteration": (_I, [_I, _VP, _VP, _VP, _VP, _VP, _I,
-                            ctypes.POINTER(Problem), _VP]),
-    "fdns_iteration_supported": (_I, [_I, _I, ctypes.POINTER(Problem)]),
-    "fdns_iteration_sync_words": (_I, []),
-    "fdns_set_fused_iteration": (_I, [_I]),
     "fdns_set_kernel_path": (None, [_I]),
     "fdns_set_tiled_grid": (None, [_I]),
     "fdns_set_pdl": (None, [_I]),
+    "fdns_set_prefetch": (None, [_I]),
+    "fdns_set_rounds": (None, [_I]),
     "fdns_debug_trace": (_I, [_I, ctypes.POINTER(ctypes.c_uint64), _I]),
     "fdns_diag_partials_size": (_I, [ctypes.POINTER(Problem)]),
     "fdns_reduce_diag": (_I, [_VP, _VP, _VP, _VP, ctypes.POINTER(Problem),

@@ -19,7 +19,6 @@
 #include "../../include/fdns_b200.h"
 #include "fdns_math.cuh"
 #include "fdns_tiled.cuh"
-#include "fdns_sn2.cuh"
 #include "fdns_tiled12.cuh"
 
 #include <cudaTypedefs.h>
@@ -30,7 +29,7 @@ using namespace fdns;
 namespace {
 
 thread_local std::string g_err;
-int g_kernel_path = 0;        // test hook: 0 default, 1 point kernels, 2 8-warp SN, 3 two-group SN,
+int g_kernel_path = 0;        // test hook: 0 default, 1 point kernels, 2 8-warp SN,
                               // 4 eager-local SN, 5 12-warp SN
 int g_tiled_ctas = 0;         // test hook: force the tiled grid size (0 = one per SM)
 std::atomic<long long> g_launches{0};
@@ -80,6 +79,13 @@ Geom make_geom(const fdns_problem* pb) {
   g.s0 = P1 * P2;
   g.fs = (int64_t)(g.n0 + 2 * g.h) * g.s0;
   return g;
+}
+
+// Whether two bundles of na / nb padded fields overlap in memory.
+bool overlaps(const double* a, int na, const double* b, int nb, const Geom& g) {
+  if (!a || !b) return false;
+  const double *ae = a + na * g.fs, *be = b + nb * g.fs;
+  return a < be && b < ae;
 }
 
 int validate(const fdns_problem* pb) {
@@ -616,15 +622,33 @@ bool saved_map(CUtensorMap* m, const double* saved, const Geom& g, int box_j = t
   return r == CUDA_SUCCESS;
 }
 
-int g_num_sms = 0;
+// Per-device state: a process may drive several GPUs (one per thread or
+// in turn), so every cache below is keyed by the current device.
+constexpr int MAX_DEVICES = 64;
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 || dev >= MAX_DEVICES ? 0 : dev;
+}
 int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  static std::atomic<int> sms[MAX_DEVICES];
+  const int dev = current_device();
+  int n = sms[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    sms[dev].store(n, std::memory_order_relaxed);
   }
-  return g_num_sms;
+  return n;
+}
+// Run `set` (a kernel's function attributes) once per device for the
+// instantiation that owns `flags`.
+template <class F>
+void once_per_device(std::atomic<uint64_t>& flags, F set) {
+  const uint64_t bit = 1ull << current_device();
+  if (flags.load(std::memory_order_acquire) & bit) return;
+  set();
+  flags.fetch_or(bit, std::memory_order_acq_rel);
 }
 
 // Persistent grid: one CTA per SM with at least ~4 plane steps each, split
@@ -769,7 +793,7 @@ struct Launch { int64_t ctas; int aligned; const int64_t* cuts; };
 // size, so only SS/RS from 256 planes use it.  FDNS_ROUNDS=C overrides the
 // unit (0 disables).
 constexpr int ROUND_PLANES = 64;
-const int g_rounds_env = std::getenv("FDNS_ROUNDS") ? std::atoi(std::getenv("FDNS_ROUNDS")) : -1;
+int g_rounds_env = std::getenv("FDNS_ROUNDS") ? std::atoi(std::getenv("FDNS_ROUNDS")) : -1;
 inline int rounds_planes(int variant, int nplanes) {
   if (variant != FDNS_SS && variant != FDNS_RS) return 0;
   const int c = g_rounds_env >= 0 ? g_rounds_env : ROUND_PLANES;
@@ -784,11 +808,13 @@ Launch pick_launch(int ntk, int ntj, int planes, int wrap, int variant, cudaStre
   if (g_tiled_ctas > 0)
     return {std::min<int64_t>(g_tiled_ctas, total), tiled::SPLIT_ALIGNED, nullptr};
   const TileCost tc{ntk, ntj, (wrap & 4) != 0, (wrap & 2) != 0, edge_scale(variant)};
-  using Key = std::tuple<int, int, int, int, int>;
+  using Key = std::tuple<int, int, int, int, int, int>;
   static std::map<Key, Launch> cache;
   static std::mutex mu;   // ctypes releases the GIL: calls may be concurrent
   std::lock_guard<std::mutex> lock(mu);
-  const Key key{ntk, ntj, planes, (wrap & 6) | (allow_table ? 8 : 0), variant};
+  // per device: the cut table is a device allocation of that GPU
+  const Key key{ntk, ntj, planes, (wrap & 6) | (allow_table ? 8 : 0), variant,
+                current_device()};
   const auto hit = cache.find(key);
   if (hit != cache.end()) return hit->second;
   const int64_t sms = (int64_t)num_sms() * ctas_per_sm;
@@ -832,16 +858,19 @@ Launch pick_launch(int ntk, int ntj, int planes, int wrap, int variant, cudaStre
   return best;
 }
 
-// A/B switch for experiments: FDNS_NO_SAVED_PREFETCH=1 disables the L2
-// prefetch of the saved state.
-const bool g_prefetch_saved = std::getenv("FDNS_NO_SAVED_PREFETCH") == nullptr;
+// Kill switches of the L2 prefetches the producer thread issues (also A/B
+// switches for experiments): FDNS_NO_SAVED_PREFETCH=1 disables the prefetch
+// of the saved state, FDNS_NO_GRAD_PREFETCH=1 that of SS/RS's nine stored
+// gradients (fdns_set_prefetch overrides both at run time).
+bool g_prefetch_saved = std::getenv("FDNS_NO_SAVED_PREFETCH") == nullptr;
+bool g_prefetch_grad = std::getenv("FDNS_NO_GRAD_PREFETCH") == nullptr;
 
 template <int V, int MODE, bool LAZY = true>
 int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, double* out,
                    const double* work,
                    const Coef& k, const Geom& g, double coef, int wrap, int i_lo, int i_hi,
                    cudaStream_t s) {
-  constexpr bool gb = (V == FDNS_SS || V == FDNS_RS) && MODE != 2;
+  constexpr bool gb = (V == FDNS_SS || V == FDNS_RS);
   constexpr int smem = V == FDNS_SN ? tiled::SMEM_BYTES_SN
                                     : (gb ? tiled::SMEM_BYTES_SS : tiled::SMEM_BYTES);
   CUtensorMap mg = m, ms = m, mp = m;
@@ -851,9 +880,10 @@ int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, 
   // saved state != stage input (RK stages 2 and 3): prefetch it into L2
   int pf = 0;
   if constexpr (MODE == 1)
-    pf = (g_prefetch_saved && saved != in && saved_map(&ms, saved, g)) ? 1 : 0;
-  static std::once_flag attr;
-  std::call_once(attr, [] {
+    pf = (g_prefetch_saved && saved != in && saved_map(&ms, saved, g)) ? tiled::PF_SAVED : 0;
+  if constexpr (gb) pf |= g_prefetch_grad ? tiled::PF_GRAD : 0;
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [] {
     cudaFuncSetAttribute(tiled::k_stage_tiled<V, MODE, LAZY>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   });
@@ -863,165 +893,22 @@ int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, 
   const int64_t total = (int64_t)ntk * ntj * nplanes;
   if constexpr (V == FDNS_SS || V == FDNS_RS) {
     if (const int c = rounds_planes(V, nplanes)) {
-      static std::once_flag attr_rr;
-      std::call_once(attr_rr, [] {
-        cudaFuncSetAttribute(tiled::k_stage_tiled<V, MODE, LAZY, false, true>,
+      static std::atomic<uint64_t> attr_rr{0};
+      once_per_device(attr_rr, [] {
+        cudaFuncSetAttribute(tiled::k_stage_tiled<V, MODE, LAZY, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       });
-      launch_pdl(tiled::k_stage_tiled<V, MODE, LAZY, false, true>,
+      launch_pdl(tiled::k_stage_tiled<V, MODE, LAZY, true>,
                  dim3((unsigned)std::min<int64_t>(num_sms(), total / c)), dim3(tiled::NT), smem,
                  s, m, mg, ms, mp, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, c,
-                 (int)tiled::SPLIT_ROUNDS, pf, (const int64_t*)nullptr, m, m,
-                 tiled::FusedArgs{});
+                 (int)tiled::SPLIT_ROUNDS, pf, (const int64_t*)nullptr);
       return 0;
     }
   }
   const Launch L = pick_launch(ntk, ntj, nplanes, wrap, V, s);
   launch_pdl(tiled::k_stage_tiled<V, MODE, LAZY>, dim3((unsigned)L.ctas), dim3(tiled::NT), smem, s,
              m, mg, ms, mp, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes,
-             L.aligned, pf, L.cuts, m, m, tiled::FusedArgs{});
-  return 0;
-}
-
-// Fused RK3 iteration (SN 8-warp / RA tiled kernel, one periodic GPU): one
-// cooperative launch runs the three stages X -> Y -> Z -> X with per-CTA
-// neighbourhood waits between them (fdns_tiled.cuh: FusedArgs).  Same split
-// and same per-point arithmetic as three fdns_stage launches, so bitwise
-// equal to them.
-inline bool use_t12(const Geom& g);
-// Off by default: bitwise equal, but measured slower than three PDL launches
-// (SN 64^3: 94.4 vs 90.1 us per step; RA 128^3: 830 vs 818 us): the
-// memory-flag hand-off between stages (publisher fence + polled L2 flags +
-// acquire fence) takes ~2-4 us after the last neighbour finishes, more than
-// the ~1.2 us programmatic-launch gap it replaces (tools/trace_fused.py,
-// DESIGN.md 3.4).  FDNS_FUSED_ITERATION=1 or fdns_set_fused_iteration(1).
-bool g_fused_iteration = std::getenv("FDNS_FUSED_ITERATION") != nullptr;
-
-bool iteration_supported(int variant, int wrap, const Geom& g) {
-  if (!g_fused_iteration || wrap != 7 || g_tiled_ctas > 0) return false;
-  if (g.n2 % tiled::TK != 0 || g.n1 % tiled::TJ != 0 || g.h != 2) return false;
-  if (((g.n2 + 2 * g.h) * 8) % 16 != 0) return false;   // TMA row pitch
-  if (variant == FDNS_RA) return g_kernel_path == 0;
-  if (variant == FDNS_SN)
-    return g_kernel_path == 2 || (g_kernel_path == 0 && !use_t12(g));
-  return false;
-}
-
-// Dependency lists of a fused iteration (device buffer, cached per
-// geometry/split): CTA b waits, before stage s > 0, for every other CTA
-// owning a (tile, plane) step its TMA boxes read -- the 3 x 3 torus
-// neighbourhood of each of its tiles, planes -2..+2 around each segment,
-// periodic along axis 0.  Layout: [G+1] offsets (relative to the array
-// start), then the CTA ids.
-const int* fused_deps(int ntk, int ntj, int planes, int variant, const Launch& L,
-                      bool may_alloc) {
-  using Key = std::tuple<int, int, int, int, int64_t, int>;
-  static std::map<Key, int*> cache;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
-  const Key key{ntk, ntj, planes, variant, L.ctas, L.aligned};
-  const auto hit = cache.find(key);
-  if (hit != cache.end()) return hit->second;
-  if (!may_alloc) return nullptr;   // never cudaMalloc inside a graph capture
-  const int64_t G = L.ctas;
-  const int64_t total = (int64_t)ntk * ntj * planes;
-  std::vector<int64_t> cuts;
-  if (L.aligned == tiled::SPLIT_TABLE) {
-    const TileCost tc{ntk, ntj, true, true, edge_scale(variant)};
-    cuts = table_cuts(G, tc, planes);
-  }
-  std::vector<int64_t> beg(G), end(G);
-  for (int64_t b = 0; b < G; ++b) {
-    const tiled::Segments S = tiled::Segments::partition(b, G, total, planes, L.aligned,
-                                                         cuts.empty() ? nullptr : cuts.data());
-    beg[b] = S.beg;
-    end[b] = S.end;
-  }
-  auto owner = [&](int64_t x) {   // largest b with beg[b] <= x
-    return (int64_t)(std::upper_bound(beg.begin(), beg.end(), x) - beg.begin()) - 1;
-  };
-  std::vector<int> out(G + 1, 0);
-  std::vector<int> ids;
-  for (int64_t b = 0; b < G; ++b) {
-    out[b] = (int)(G + 1 + ids.size());
-    std::vector<int> mine;
-    const tiled::Segments S{beg[b], end[b], planes};
-    for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) {
-      const int64_t se = S.seg_end(x), tile = x / planes;
-      const int kt = (int)(tile % ntk), jt = (int)(tile / ntk);
-      const int p0 = (int)(x % planes) - 2, p1 = (int)((se - 1) % planes) + 2;
-      for (int dj = -1; dj <= 1; ++dj)
-        for (int dk = -1; dk <= 1; ++dk) {
-          const int64_t tn = (int64_t)((jt + dj + ntj) % ntj) * ntk + (kt + dk + ntk) % ntk;
-          auto add = [&](int a, int c) {   // planes [a, c] of tile tn
-            for (int64_t o = owner(tn * planes + a); o <= owner(tn * planes + c); ++o)
-              if (o != b && beg[o] < end[o]) mine.push_back((int)o);
-          };
-          if (p1 - p0 + 1 >= planes) add(0, planes - 1);
-          else if (p0 < 0) { add(p0 + planes, planes - 1); add(0, p1); }
-          else if (p1 >= planes) { add(p0, planes - 1); add(0, p1 - planes); }
-          else add(p0, p1);
-        }
-    }
-    std::sort(mine.begin(), mine.end());
-    mine.erase(std::unique(mine.begin(), mine.end()), mine.end());
-    ids.insert(ids.end(), mine.begin(), mine.end());
-  }
-  out[G] = (int)(G + 1 + ids.size());
-  out.insert(out.end(), ids.begin(), ids.end());
-  int* d = nullptr;
-  if (cudaMalloc(&d, out.size() * sizeof(int)) != cudaSuccess ||
-      cudaMemcpy(d, out.data(), out.size() * sizeof(int), cudaMemcpyHostToDevice) !=
-          cudaSuccess) {
-    cudaGetLastError();
-    if (d) cudaFree(d);
-    return nullptr;
-  }
-  cache[key] = d;
-  return d;
-}
-
-template <int V>
-int launch_iteration_v(double* X, double* Y, double* Z, unsigned* sync, const double* coefs,
-                       const Coef& k, const Geom& g, cudaStream_t s) {
-  constexpr int smem = V == FDNS_SN ? tiled::SMEM_BYTES_SN : tiled::SMEM_BYTES;
-  CUtensorMap m0, m1, m2, ms;
-  if (!plane_map(&m0, X, g) || !plane_map(&m1, Y, g) || !plane_map(&m2, Z, g))
-    return fail("plane tensor map");
-  ms = m0;
-  const int pf = (g_prefetch_saved && saved_map(&ms, X, g)) ? 1 : 0;
-  static std::once_flag attr;
-  std::call_once(attr, [] {
-    cudaFuncSetAttribute(tiled::k_stage_tiled<V, 1, true, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  });
-  const int ntk = g.n2 / tiled::TK, ntj = g.n1 / tiled::TJ;
-  const int64_t total = (int64_t)ntk * ntj * g.n0;
-  const Launch L = pick_launch(ntk, ntj, g.n0, 7, V, s);
-  if (L.ctas > num_sms() || L.ctas > tiled::FUSED_SYNC_WORDS - 2)
-    return fail("fused iteration: more CTAs than SMs");
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(s, &cs);
-  const int* deps = fused_deps(ntk, ntj, g.n0, V, L, cs == cudaStreamCaptureStatusNone);
-  if (!deps) return fail("fused iteration: dependency lists unavailable "
-                         "(allocated on the first eager call, not during graph capture)");
-  const tiled::FusedArgs fa{Z, X, coefs[1], coefs[2], sync, deps};
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)L.ctas);
-  cfg.blockDim = dim3(tiled::NT);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;   // every CTA co-resident (they wait on each other)
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  static const bool coop = std::getenv("FDNS_FUSED_NOCOOP") == nullptr;   // A/B only
-  cfg.numAttrs = coop ? 1 : 0;
-  const cudaError_t e = cudaLaunchKernelEx(
-      &cfg, tiled::k_stage_tiled<V, 1, true, true>, m0, m0, ms, m0, (const double*)nullptr,
-      (const double*)X, Y, k, g, coefs[0], ntk, total, 7, 0, g.n0, L.aligned, pf, L.cuts, m1, m2,
-      fa);
-  if (e != cudaSuccess) return fail("fused iteration launch", e);
+             L.aligned, pf, L.cuts);
   return 0;
 }
 
@@ -1044,8 +931,8 @@ int launch_t12(const double* in, const double* saved, double* out, const Coef& k
   int pf = 0;
   if constexpr (MODE == 1)
     pf = (g_prefetch_saved && saved != in && saved_map(&ms, saved, g, L::TJ)) ? 1 : 0;
-  static std::once_flag attr;
-  std::call_once(attr, [] {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [] {
     cudaFuncSetAttribute(t12::k_stage_t12<FDNS_SN, MODE, TJ_>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_BYTES);
     if (L::MINB > 1)
@@ -1065,24 +952,6 @@ int launch_t12(const double* in, const double* saved, double* out, const Coef& k
 }
 
 template <int MODE>
-int launch_sn2(const CUtensorMap& m, const double* saved, double* out, const Coef& k,
-               const Geom& g, double coef, int wrap, int i_lo, int i_hi, cudaStream_t s) {
-  static std::once_flag attr;
-  std::call_once(attr, [] {
-    cudaFuncSetAttribute(sn2::k_stage_sn2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         sn2::SMEM_BYTES);
-  });
-  const int ntk = (g.n2 + tiled::TK - 1) / tiled::TK;
-  const int ntj = (g.n1 + tiled::TJ - 1) / tiled::TJ;
-  const int nplanes = i_hi - i_lo;
-  const int64_t total = (int64_t)ntk * ntj * nplanes;
-  const Launch L = pick_launch(ntk, ntj, nplanes, wrap, FDNS_SN, s, false);
-  launch_pdl(sn2::k_stage_sn2<MODE>, dim3((unsigned)L.ctas), dim3(sn2::NT), sn2::SMEM_BYTES, s,
-             m, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes, L.aligned);
-  return 0;
-}
-
-template <int MODE>
 int launch_residual(int variant, const double* in, const double* saved, double* out,
                     double* work, const Coef& k, const Geom& g, double coef, int wrap,
                     int i_lo, int i_hi, cudaStream_t s) {
@@ -1094,8 +963,7 @@ int launch_residual(int variant, const double* in, const double* saved, double* 
       case FDNS_RA: rc = launch_tiled_v<FDNS_RA, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
       case FDNS_RS: rc = launch_tiled_v<FDNS_RS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
       case FDNS_SN:
-        if (g_kernel_path == 3) rc = launch_sn2<MODE>(m, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
-        else if (g_kernel_path == 5 || (g_kernel_path == 0 && use_t12(g)))
+        if (g_kernel_path == 5 || (g_kernel_path == 0 && use_t12(g)))
           rc = launch_t12<MODE>(in, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
         else if (g_kernel_path == 4)
           rc = launch_tiled_v<FDNS_SN, MODE, false>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
@@ -1145,8 +1013,6 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
     else k_diag_ghost<<<nb, 256, 0, s>>>(in, d0, d1p, d2p, k, g, f0, f1, f2);
   };
   if (variant == FDNS_BL) {
-    // (a TMA-staged fill, k_stage_tiled<BL, 2>, measured 1.6x slower at
-    // 256^3: 8 warps/SM cannot keep 54 store streams in flight)
     launch_pdl(k_fill_bl_all, grd, blk, 0, s, in, work, k, g);
     ghosts(work + slot(0, S_U + 0) * g.fs, work + slot(1, S_U + 1) * g.fs,
            work + slot(2, S_U + 2) * g.fs, true);
@@ -1198,6 +1064,13 @@ void fdns_set_tiled_grid(int32_t ctas) { g_tiled_ctas = ctas; }
 
 void fdns_set_pdl(int32_t enabled) { g_pdl = enabled != 0; }
 
+void fdns_set_rounds(int32_t planes) { g_rounds_env = planes; }
+
+void fdns_set_prefetch(int32_t mask) {
+  g_prefetch_saved = (mask & 1) != 0;
+  g_prefetch_grad = (mask & 2) != 0;
+}
+
 int32_t fdns_debug_trace(int32_t enable, uint64_t* out, int32_t n) {
   int on = enable;
   if (cudaMemcpyToSymbol(tiled::g_trace_on, &on, sizeof(int)) != cudaSuccess)
@@ -1206,14 +1079,6 @@ int32_t fdns_debug_trace(int32_t enable, uint64_t* out, int32_t n) {
     unsigned zero = 0;
     if (cudaMemcpyToSymbol(tiled::g_trace_n, &zero, sizeof(zero)) != cudaSuccess)
       return fail("trace log reset", cudaGetLastError());
-  }
-  if (out && n > 0 && enable == 4) {   // fused-iteration timeline (debug)
-    const int m = std::min(n, tiled::TRACE_CTAS * tiled::FTRACE_W);
-    if (cudaMemcpyFromSymbol(out, tiled::g_ftrace, m * sizeof(uint64_t)) != cudaSuccess)
-      return fail("trace copy", cudaGetLastError());
-    on = 0;
-    cudaMemcpyToSymbol(tiled::g_trace_on, &on, sizeof(int));
-    return 0;
   }
   if (out && n > 0 && enable == 3) {   // read the launch log: [count, records...]
     unsigned cnt = 0;
@@ -1306,6 +1171,9 @@ int32_t fdns_residual(int32_t variant, const double* state, double* work, double
   if (nw < 0) return fail("unknown variant");
   if (nw > 0 && !work) return fail("variant needs work arrays");
   const Geom g = make_geom(pb);
+  if (overlaps(out, 5, state, NFIELDS, g) || (nw > 0 && (overlaps(work, nw, state, NFIELDS, g) ||
+                                                         overlaps(work, nw, out, 5, g))))
+    return fail("fdns_residual: out, state and work must not overlap");
   const Coef k = make_coef(pb);
   cudaStream_t s = (cudaStream_t)stream;
   if (int e = launch_fills(variant, state, work, k, g, s)) return e;
@@ -1331,6 +1199,13 @@ int32_t fdns_stage_planes(int32_t variant, const double* in, const double* saved
   if (nw < 0) return fail("unknown variant");
   if (nw > 0 && !work) return fail("variant needs work arrays");
   if (in == out) return fail("fused stage needs distinct in/out bundles");
+  {
+    const Geom gg = make_geom(pb);
+    if (overlaps(out, NFIELDS, in, NFIELDS, gg) ||
+        (nw > 0 && (overlaps(work, nw, in, NFIELDS, gg) || overlaps(work, nw, out, NFIELDS, gg) ||
+                    overlaps(work, nw, saved, 5, gg))))
+      return fail("fused stage: in, out and work must not overlap (saved may alias out)");
+  }
   if (i_lo < 0 || i_hi > pb->n[0] || i_lo > i_hi) return fail("plane range outside the slab");
   const Geom g = make_geom(pb);
   const Coef k = make_coef(pb);
@@ -1338,38 +1213,6 @@ int32_t fdns_stage_planes(int32_t variant, const double* in, const double* saved
   if (with_fills)
     if (int e = launch_fills(variant, in, work, k, g, s)) return e;
   return launch_residual<1>(variant, in, saved, out, work, k, g, coef, wrap_mask, i_lo, i_hi, s);
-}
-
-int32_t fdns_iteration_sync_words(void) { return tiled::FUSED_SYNC_WORDS; }
-
-int32_t fdns_set_fused_iteration(int32_t enabled) {
-  const int32_t was = g_fused_iteration ? 1 : 0;
-  g_fused_iteration = enabled != 0;
-  return was;
-}
-
-int32_t fdns_iteration_supported(int32_t variant, int32_t wrap_mask, const fdns_problem* pb) {
-  if (validate(pb)) return 0;
-  return iteration_supported(variant, wrap_mask, make_geom(pb)) ? 1 : 0;
-}
-
-int32_t fdns_iteration(int32_t variant, double* X, double* Y, double* Z, uint32_t* sync,
-                       const double* coefs, int32_t wrap_mask, const fdns_problem* pb,
-                       void* stream) {
-  if (int e = validate(pb)) return e;
-  if (!X || !Y || !Z || !sync || !coefs) return fail("fdns_iteration: null pointer");
-  if (X == Y || Y == Z || X == Z) return fail("fdns_iteration needs three distinct bundles");
-  const Geom g = make_geom(pb);
-  if (!iteration_supported(variant, wrap_mask, g))
-    return fail("fdns_iteration: not supported for this variant/geometry (use fdns_stage)");
-  const Coef k = make_coef(pb);
-  cudaStream_t s = (cudaStream_t)stream;
-  const int rc = variant == FDNS_SN
-                     ? launch_iteration_v<FDNS_SN>(X, Y, Z, sync, coefs, k, g, s)
-                     : launch_iteration_v<FDNS_RA>(X, Y, Z, sync, coefs, k, g, s);
-  if (rc) return rc;
-  count();
-  return check_launch("fused iteration kernel");
 }
 
 int32_t fdns_stage(int32_t variant, const double* in, const double* saved, double* out,

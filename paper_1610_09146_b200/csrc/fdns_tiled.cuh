@@ -58,17 +58,6 @@ __device__ __forceinline__ void trace(int pt) {
     }
   }
 }
-// Fused-iteration timeline (debug, g_trace_on != 0): per CTA and stage the
-// stage start (after the neighbourhood wait), first window ready, stage end.
-constexpr int FTRACE_W = 9;
-__device__ unsigned long long g_ftrace[TRACE_CTAS * FTRACE_W];
-__device__ __forceinline__ void ftrace(int st, int pt) {
-  if (g_trace_on && threadIdx.x == 0 && blockIdx.x < TRACE_CTAS) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_ftrace[blockIdx.x * FTRACE_W + st * 3 + pt] = t;
-  }
-}
 constexpr int PK = TK + 4, PJ = TJ + 4;
 constexpr int PLANE = PK * PJ;          // doubles per field per plane slot
 constexpr int SLOT = NFIELDS * PLANE;   // doubles per plane slot
@@ -77,6 +66,9 @@ constexpr int NLOAD = 8;                // fields TMA-staged per plane (rho..u2)
 constexpr uint32_t LOAD_BYTES = NLOAD * PLANE * 8;
 constexpr int NOUT_STAGE = 8;           // fields a fused stage writes (cons + u)
 constexpr int NR = 6;                   // ring depth: 5-plane window + 1 prefetch
+// pf_saved bits of the stage kernels: L2 prefetch of the saved state / of
+// SS/RS's nine stored gradients (host kill switches, fdns_set_prefetch)
+constexpr int PF_SAVED = 1, PF_GRAD = 2;
 constexpr int SMEM_BYTES = NR * SLOT * 8 + 128;
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
@@ -389,15 +381,6 @@ struct TiledSSProvider {
   }
 };
 
-// BL work-array fill from the staged tile: the 54 plain/product derivatives
-// of one point into their arrays (plan.py:369-392).
-template <int A_, int L>
-__device__ __forceinline__ void fill_slots(const Coef& k, const SAcc& a, double* __restrict__ wa,
-                                           int64_t c, int64_t fs) {
-  wa[slot(A_, L) * fs + c] = eval_slot<A_, L>(k, a);
-  if constexpr (L + 1 < S_PER_AXIS) fill_slots<A_, L + 1>(k, a, wa, c, fs);
-}
-
 // Static, balanced work split of one stage: the (tile, plane) steps in
 // tile-major order are cut into gridDim.x equal ranges; a CTA walks its
 // range as <= a few segments (one per tile touched).  The TMA producer
@@ -490,90 +473,21 @@ struct Segments {
   }
 };
 
-// Fused RK3 iteration (one launch for the three stages of a periodic
-// one-GPU step, SN/RA): stage s reads bundle in[s] = (X, Y, Z)[s], writes
-// out[s] = (Y, Z, X)[s], saved state X.  Every CTA keeps its (tile, plane)
-// range in all three stages; before stage s > 0 it waits only for the CTAs
-// whose stage s-1 ranges cover its TMA footprint (the 3 x 3 torus
-// neighbourhood of its tiles, planes -2..+2 around its range, periodic), not
-// for the whole grid -- no launch gap and no global tail between stages.
-// Write-after-read is covered transitively: stage 2 overwrites X at a point
-// only after the stage-1 footprint CTAs finished, and they finished stage 0
-// (every TMA read of X around that point) before starting stage 1.
-// sync[0] = launch epoch, sync[1] = retired CTAs, sync[2 + b] = last stage
-// generation (3 * epoch + stage + 1) CTA b completed.  Needs every CTA
-// co-resident (cooperative launch, one CTA per SM).
-struct FusedArgs {
-  double* out1;     // stage-1 output (Z)
-  double* out2;     // stage-2 output (X, in place over the saved state)
-  double coef1, coef2;
-  unsigned* sync;
-  const int* deps;  // [G+1] offsets into the same array, then CTA ids
-};
-constexpr int FUSED_SYNC_WORDS = 2 + 4096;   // epoch, retired count, per-CTA generations
-
-__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_gpu(unsigned* p, unsigned v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Warp 0: wait until every CTA this CTA's stage-s footprint depends on has
-// published generation >= need (the dependency list is host-computed per
-// geometry: owners of the 3 x 3 torus-neighbour tiles' planes -2..+2 around
-// each of its segments, fdns_b200.cu:fused_deps), then fence (acquire for
-// the TMA loads that follow the CTA barrier).
-__device__ __forceinline__ void fused_wait(const int* __restrict__ deps,
-                                           const unsigned* done, unsigned need) {
-  const int lane = threadIdx.x & 31;
-  const int b0 = deps[blockIdx.x], b1 = deps[blockIdx.x + 1];
-  for (int i = b0 + lane; i < b1; i += 32) {
-    const unsigned* f = done + deps[i];
-    if ((int)(ld_relaxed_gpu(f) - need) >= 0) continue;
-    const long long t0 = clock64();
-    while ((int)(ld_relaxed_gpu(f) - need) < 0) {
-      if (clock64() - t0 > 4000000000LL) __trap();   // never hang the GPU
-    }
-  }
-  __syncwarp();
-  __threadfence();
-}
-
-// End of a fused launch: the last CTA to retire advances the epoch (every
-// CTA read it at entry, so no CTA of this launch can see the new value).
-__device__ __forceinline__ void fused_retire(unsigned* sync) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&sync[1], 1u) == gridDim.x - 1) {
-      atomicExch(&sync[1], 0u);
-      atomicAdd(&sync[0], 1u);
-    }
-  }
-}
-
 #ifndef FDNS_EARLY_GV
 #define FDNS_EARLY_GV 1
 #endif
 
-template <int V, int MODE, bool LAZY = true, bool FUSED = false, bool RR = false>
+template <int V, int MODE, bool LAZY = true, bool RR = false>
 __global__ void __launch_bounds__(NT, 1)
     k_stage_tiled(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tgw,
                   const __grid_constant__ CUtensorMap tsv, const __grid_constant__ CUtensorMap tgp,
                   const double* __restrict__ work,
                   const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
                   int64_t total_steps, int wrap_mask, int i_lo, int nplanes, int split,
-                  int pf_saved, const int64_t* __restrict__ cuts,
-                  const __grid_constant__ CUtensorMap tin1,
-                  const __grid_constant__ CUtensorMap tin2, FusedArgs fa) {
-  static_assert(!FUSED || ((V == FDNS_SN || V == FDNS_RA) && MODE == 1),
-                "fused iteration: SN/RA stage kernels only");
+                  int pf_saved, const int64_t* __restrict__ cuts) {
   extern __shared__ __align__(128) double sm[];
   constexpr bool kBuf = (V == FDNS_SN);
-  constexpr bool kGB = (V == FDNS_SS || V == FDNS_RS) && MODE != 2;
+  constexpr bool kGB = (V == FDNS_SS || V == FDNS_RS);
   double* bufs0 = sm + NR * SLOT;   // SN: 2 x NBUF buffer planes; SS/RS: 2 x NGB staged
   uint64_t* bars = reinterpret_cast<uint64_t*>(
       sm + NR * SLOT + (kBuf ? 2 * NBUF * PLANE : (kGB ? 2 * NGB * PLANE : 0)));
@@ -595,13 +509,7 @@ __global__ void __launch_bounds__(NT, 1)
     if constexpr (RR) return S.plane_of(x);
     else return (int)(x % nplanes);
   };
-  if (S.beg >= S.end) {
-    if constexpr (FUSED) {
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      fused_retire(fa.sync);
-    }
-    return;
-  }
+  if (S.beg >= S.end) return;
   trace(0);
 
   if (tid == 0) {
@@ -617,16 +525,10 @@ __global__ void __launch_bounds__(NT, 1)
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   trace(1);
-  // fused iteration: this launch's generation base (3 * epoch)
-  unsigned gen0 = 0;
-  if constexpr (FUSED) {
-    gen0 = 3u * ld_relaxed_gpu(fa.sync);
-    ftrace(0, 0);
-  }
-  const CUtensorMap* tmap = &tin;   // the current stage's input bundle
+  const CUtensorMap* tmap = &tin;
   double* outp = out;
-  double coefp = coef;
-  int pfp = FUSED ? 0 : pf_saved;   // stage 0 of a fused iteration: saved == input
+  const double coefp = coef;
+  const int pfp = pf_saved;
 
   // SS/RS: staged gradient box of the centre plane of step `gs`
   auto issue_gb_tile = [&](int gs, int k0, int j0, int plane) {
@@ -664,11 +566,12 @@ __global__ void __launch_bounds__(NT, 1)
     // saved state of this plane (a centre plane of the segment) into L2,
     // ~NR steps before the epilogue loads it: when it is not the stage
     // input it would otherwise come from DRAM at full latency
-    if (MODE == 1 && pfp && p_r >= 2 && p_r < p_len - 2)
+    if (MODE == 1 && (pfp & PF_SAVED) && p_r >= 2 && p_r < p_len - 2)
       tma_prefetch_l2(&tsv, p_c0 + 2, p_c1 + 2, p_plane + p_r);
     // SS/RS: the nine stored gradients of this plane's tile columns (the
     // off-diagonal loads at the centre and the axis-0 queue loads) into L2
-    if constexpr (kGB) tma_prefetch_l2(&tgp, p_c0 + 2, p_c1 + 2, p_plane + p_r);
+    if constexpr (kGB)
+      if (pfp & PF_GRAD) tma_prefetch_l2(&tgp, p_c0 + 2, p_c1 + 2, p_plane + p_r);
     ++issued;
     p_slot = p_slot + 1 == NR ? 0 : p_slot + 1;
     if (++p_r == p_len) {
@@ -689,42 +592,6 @@ __global__ void __launch_bounds__(NT, 1)
     const int x = wsl + d;
     return x >= NR ? x - NR : x;
   };
-  constexpr int NST = FUSED ? 3 : 1;
-#pragma unroll 1
-  for (int st = 0; st < NST; ++st) {
-  if constexpr (FUSED) {
-    if (st > 0) {
-      // publish stage st-1, wait for the footprint's owners, switch bundles
-      __syncthreads();
-      ftrace(st - 1, 2);
-      if (tid == 0) {
-#ifndef FDNS_FUSED_NOFENCE
-        __threadfence();
-#endif
-        st_relaxed_gpu(fa.sync + 2 + blockIdx.x, gen0 + (unsigned)st);
-      }
-#ifndef FDNS_FUSED_NOWAIT
-      if (tid < 32) fused_wait(fa.deps, fa.sync + 2, gen0 + (unsigned)st);
-#endif
-      __syncthreads();
-      ftrace(st, 0);
-      tmap = st == 1 ? &tin1 : &tin2;
-      outp = st == 1 ? fa.out1 : fa.out2;
-      coefp = st == 1 ? fa.coef1 : fa.coef2;
-      pfp = pf_saved;
-      if (tid == 0) {
-#ifndef FDNS_FUSED_NOPROXY
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-#endif
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        p_seg = S.beg;
-        p_r = 0;
-        enter_segment();
-        total_pos += stage_pos;
-        while (issued < total_pos && issued < w + NR) issue_next();
-      }
-    }
-  }
   for (int64_t x = S.beg; x < S.end; x = seg_next(x)) {
     const int64_t se = S.seg_end(x);
     const int64_t tile = tile_at(x);
@@ -827,9 +694,6 @@ __global__ void __launch_bounds__(NT, 1)
       }
       __syncthreads();
       if (w == 0) trace(2);
-      if constexpr (FUSED) {
-        if (t == 0 && x == S.beg) ftrace(st, 1);
-      }
       if (tid == 0) {
         if (issued < total_pos && issued < w + NR) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -867,16 +731,6 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
 
-      if constexpr (MODE == 2) {   // BL fill: derivative arrays only
-        if (active) {
-          const int64_t c = (int64_t)(i + g.h) * g.s0 + (int64_t)(jj + g.h) * g.s1 + (kk + g.h);
-          double* wa = const_cast<double*>(work);
-          fill_slots<0, 0>(k, a, wa, c, g.fs);
-          fill_slots<1, 0>(k, a, wa, c, g.fs);
-          fill_slots<2, 0>(k, a, wa, c, g.fs);
-        }
-        continue;
-      }
       double r[NFIELDS];
 #pragma unroll
       for (int f = 0; f < NFIELDS; ++f) r[f] = a.v(f, 0, 0, 0);   // r[RHOE_F] = rho*e
@@ -936,12 +790,6 @@ __global__ void __launch_bounds__(NT, 1)
     }
     w += 4;   // the segment's trailing positions
     wsl = w % NR;
-  }
-  }   // stages
-  if constexpr (FUSED) {
-    __syncthreads();
-    ftrace(2, 2);
-    fused_retire(fa.sync);
   }
   trace(3);
 }

@@ -11,8 +11,6 @@ hand-written sm_100a kernel path runs (csrc/fdns_math.cuh providers).
 
 from __future__ import annotations
 
-import ctypes
-
 from dataclasses import dataclass
 
 import torch
@@ -358,36 +356,6 @@ class ResidualEvaluator:
             self._workspace = (alloc_bundle(self.grid, 10),
                                alloc_bundle(self.grid, 10))
         return self._workspace
-
-    @property
-    def fused_iteration(self) -> bool:
-        """Whether a whole RK3 iteration runs as one launch here (opt-in,
-        fdns_set_fused_iteration; SN on the 8-warp kernel / RA, one
-        periodic GPU, grid tiled by 32x8 columns).  Decided on first use:
-        set the library hooks before creating the evaluator."""
-        if getattr(self, "_fused_ok", None) is None:
-            self._fused_ok = bool(self.lib.fdns_iteration_supported(
-                self.plan.variant_id, self.wrap_mask, self.problem))
-        return self._fused_ok
-
-    def iteration(self, X: torch.Tensor, Y: torch.Tensor, Z: torch.Tensor,
-                  coefs) -> None:
-        """The three fused stages X -> Y -> Z -> X in one launch
-        (fdns_iteration); bitwise equal to three `stage` calls."""
-        if getattr(self, "_sync", None) is None:
-            self._sync = torch.zeros(int(self.lib.fdns_iteration_sync_words()),
-                                     dtype=torch.int32, device=X.device)
-            self._coefs = None
-        key = tuple(float(c) for c in coefs)
-        if self._coefs is None or self._coefs[0] != key:
-            # host array kept alive with the evaluator (read at launch time)
-            arr = (ctypes.c_double * 3)(*key)
-            self._coefs = (key, arr)
-        _lib.check(self.lib.fdns_iteration(
-            self.plan.variant_id, _lib.ptr(X), _lib.ptr(Y), _lib.ptr(Z),
-            _lib.ptr(self._sync), ctypes.cast(self._coefs[1], ctypes.c_void_p),
-            self.wrap_mask, self.problem, _lib.stream_handle()),
-            f"iteration ({self.plan.name})")
 
     @property
     def wrap_mask(self) -> int:

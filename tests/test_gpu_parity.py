@@ -208,6 +208,65 @@ def test_c3_perturbed_128_200_steps(golden_meta, variant):
         assert abs(rec.enstrophy - row[2]) <= 1e-10 * abs(row[2])
 
 
+def _check_history(rep, ref, tol=1e-10):
+    assert len(rep.records) == len(ref["history"])
+    for rec, row in zip(rep.records, ref["history"]):
+        assert rec.time == pytest.approx(row[0], rel=1e-15, abs=1e-15)
+        assert abs(rec.kinetic_energy - row[1]) <= tol * abs(row[1])
+        assert abs(rec.enstrophy - row[2]) <= tol * abs(row[2])
+        assert abs(rec.total_mass - row[3]) <= tol * abs(row[3])
+        assert abs(rec.total_energy - row[7]) <= tol * abs(row[7])
+
+
+def _free_device():
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("variant", ["RA", "SS"])
+def test_c4_tgv256_100_steps(golden_meta, variant):
+    """Config C4 (BASELINE.json configs[3]): TGV 256^3, dt=8.5e-4, 100 RK3
+    steps, the RA and SS variants on one GPU -- final fields bitwise equal
+    to the reference's (hashes generated by the reference itself,
+    tests/golden/make_golden.py --large), KE/enstrophy/mass/energy sampled
+    every 10 steps within 1e-10."""
+    ref = golden_meta["c4_tgv256"]
+    g = grid_of((256,) * 3)
+    state = fd.taylor_green_init(g, C)
+    assert abs(fd.mean_density(state) - ref["rho0"]) <= 1e-13 * ref["rho0"]
+    ev = fd.ResidualEvaluator(g, C, variant)
+    rep = fd.run(state, fd.RKScheme(dt=8.5e-4), ev, 100, cadence=10,
+                 collect=fd.make_collector(g, ref["rho0"]))
+    assert [sha(f) for f in host_cons(state)] == ref["sha256"]
+    _check_history(rep, ref)
+    del state, ev
+    _free_device()
+
+
+@pytest.mark.parametrize("variant", NS_VARIANTS)
+def test_c5_tgv512_matches_reference(golden_meta, variant):
+    """Config C5 (BASELINE.json configs[4]): TGV 512^3 on one GPU (BL's 90
+    padded fields ~99 GB of HBM), dt=4.2e-4, 2 RK3 steps -- the most the
+    reference itself can run in the build container (62 GB host RAM) --
+    every variant's final fields bitwise equal to the reference's, the
+    diagnostics of every step within 1e-10.  A common-mode addressing bug at
+    the bench's own size would show up here, not only in cross-variant
+    agreement."""
+    ref = golden_meta["c5_tgv512"]
+    g = grid_of((512,) * 3)
+    state = fd.taylor_green_init(g, C)
+    ev = fd.ResidualEvaluator(g, C, variant)
+    rep = fd.run(state, fd.RKScheme(dt=4.2e-4), ev, 2, cadence=1,
+                 collect=fd.make_collector(g, ref["rho0"]))
+    got = host_cons(state)
+    assert [sha(f) for f in got] == ref["sha256"]
+    assert [float(np.max(np.abs(f))) for f in got] == ref["absmax"]
+    _check_history(rep, ref)
+    del state, ev, got
+    _free_device()
+
+
 @pytest.mark.parametrize("variant", ["BL", "RA", "RS", "SN", "SS"])
 def test_analytic_rhs_convergence(variant):
     """Known answer (test_plan.py:207-238): rho = 1, u = (sin x, 0, 0),
@@ -397,61 +456,6 @@ def kernel_path():
     yield lib
     lib.fdns_set_kernel_path(0)
     lib.fdns_set_tiled_grid(0)
-    lib.fdns_set_fused_iteration(0)
-
-
-def _run_fields(lib, variant, npts, cons, steps, fused, dt=1e-3):
-    lib.fdns_set_fused_iteration(int(fused))
-    g = grid_of(npts)
-    st = state_from_cons(g, cons)
-    ev = fd.ResidualEvaluator(g, C, variant)
-    assert ev.fused_iteration == (fused and variant in ("SN", "RA")
-                                  and npts[2] % 32 == 0 and npts[1] % 8 == 0
-                                  and not (variant == "SN" and npts[1] >= 96))
-    fd.run(st, fd.RKScheme(dt=dt), ev, steps)
-    torch.cuda.synchronize()
-    return st.bundle.cpu().numpy()
-
-
-@pytest.mark.parametrize("variant", ["SN", "RA"])
-@pytest.mark.parametrize("npts", [(5, 8, 32), (20, 16, 64), (64, 24, 96),
-                                  (128, 64, 64), (7, 64, 32)])
-def test_one_launch_iteration_equals_three_stages(kernel_path, variant, npts):
-    """fdns_iteration (the three stages in one cooperative launch, CTAs
-    waiting only on their stencil neighbourhood) is bitwise equal to three
-    fdns_stage launches -- whole padded bundles, ghosts included -- over
-    three RK3 steps, on geometries whose CTA ranges wrap planes, span tiles
-    or hold fewer planes than the stencil reach."""
-    F = npo.perturbed_taylor_green(max(npts), CO, 11)
-    cons = np.ascontiguousarray(
-        npo.interior(F[:5], 2)[:, :npts[0], :npts[1], :npts[2]])
-    want = _run_fields(kernel_path, variant, npts, cons, 3, False)
-    got = _run_fields(kernel_path, variant, npts, cons, 3, True)
-    assert np.array_equal(got, want)
-
-
-def test_one_launch_iteration_repeatable_and_counted(kernel_path):
-    """The fused 64^3 SN/RA iteration: one launch per RK3 step, and twenty
-    repeated 3-step runs (epochs advancing through the sync words) all
-    bitwise equal to the three-launch result (a missing neighbourhood wait
-    would show up as run-to-run differences)."""
-    n = 64
-    F = npo.taylor_green(n, CO)
-    cons = npo.interior(F[:5], 2)
-    for variant in ("SN", "RA"):
-        want = _run_fields(kernel_path, variant, (n,) * 3, cons, 3, False)
-        kernel_path.fdns_set_fused_iteration(1)
-        g = grid_of((n,) * 3)
-        ev = fd.ResidualEvaluator(g, C, variant)
-        assert ev.fused_iteration
-        for rep in range(20):
-            st = state_from_cons(g, cons)
-            c0 = kernel_path.fdns_launch_count()
-            fd.run(st, fd.RKScheme(dt=1e-3), ev, 3)
-            torch.cuda.synchronize()
-            # 3 iterations + the primitives before and after the loop
-            assert kernel_path.fdns_launch_count() - c0 == 3 + 2
-            assert np.array_equal(st.bundle.cpu().numpy(), want), (variant, rep)
 
 
 @pytest.mark.parametrize("variant,path", [(v, 0) for v in VARIANTS] + [("SN", 5)])
@@ -481,16 +485,16 @@ def test_tiled_segment_transitions(kernel_path, variant, ctas, path):
 
 @pytest.mark.parametrize("ctas", [0, 5])
 def test_sn_kernel_families_agree(kernel_path, ctas):
-    """SN on one warp group with lazily evaluated derivatives (default), with
-    the eager local array (path 4), on two warp groups (path 3), on the
-    8-warp (path 2) and 12-warp (path 5) tiled kernels and on the point
-    kernels (path 1): bitwise equal after two RK3 steps."""
+    """SN with lazily evaluated derivatives (default), with the eager local
+    array (path 4), on the 8-warp (path 2) and 12-warp (path 5) tiled
+    kernels and on the point kernels (path 1): bitwise equal after two RK3
+    steps."""
     npts = (19, 24, 40)
     F = npo.manufactured(npts, CO)
     g = grid_of(npts)
     cons = npo.interior(F[:5], 2)
     finals = []
-    for path in (1, 2, 3, 4, 5, 0):
+    for path in (1, 2, 4, 5, 0):
         kernel_path.fdns_set_kernel_path(path)
         kernel_path.fdns_set_tiled_grid(ctas)
         st = state_from_cons(g, cons)
