@@ -58,6 +58,13 @@ int32_t fdns_workarray_count(int32_t variant);
  * eval_primitives_grouped (physics.py:169-202). */
 int32_t fdns_primitives(double* state, const fdns_problem* pb, void* stream);
 
+/* The same on padded axis-0 planes [p_lo, p_hi) only (0 <= p_lo <= p_hi <=
+ * n0+2h): a z-slab rank forms u, p, T of its ghost planes after receiving
+ * their conservative fields (decomp.py), the values the sending rank's
+ * stage kernel computed with the same expressions. */
+int32_t fdns_primitives_planes(double* state, int32_t p_lo, int32_t p_hi,
+                               const fdns_problem* pb, void* stream);
+
 /* Periodic ghost fill of nf consecutive fields along the axes in axes_mask
  * (bit a = axis a) -- replaces mesh.halo_exchange (mesh.py:118-139). */
 int32_t fdns_halo_wrap(double* fields, int32_t nf, int32_t axes_mask,

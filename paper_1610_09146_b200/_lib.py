@@ -45,6 +45,7 @@ EXPORTS = {
     "fdns_launch_count": (ctypes.c_int64, []),
     "fdns_workarray_count": (_I, [_I]),
     "fdns_primitives": (_I, [_VP, ctypes.POINTER(Problem), _VP]),
+    "fdns_primitives_planes": (_I, [_VP, _I, _I, ctypes.POINTER(Problem), _VP]),
     "fdns_halo_wrap": (_I, [_VP, _I, _I, ctypes.POINTER(Problem), _VP]),
     "fdns_residual": (_I, [_I, _VP, _VP, _VP, ctypes.POINTER(Problem), _VP]),
     "fdns_rk_update": (_I, [_VP, _VP, _VP, ctypes.c_double,

@@ -6,9 +6,12 @@ method of bench.py:51-71: fresh Taylor-Green state per cell, two untimed
 warm-up iterations, the timed `run`'s `loop_seconds`, minimum over
 repeats), `speedup_rows`, `write_bench_csv`, `write_speedup_csv`
 (bench.py:91-126), `ScalingRecord` and `write_scaling_csv`
-(bench.py:129-205).  One process drives one GPU, so scaling tables are
-assembled from per-N runs (`bench.py --gpus N` lines) with
-`scaling_records`.
+(bench.py:129-205), and the scaling drivers `strong_scaling`,
+`weak_scaling` and `decompose_workers` (bench.py:138-196) with GPUs in
+place of threads: one process drives one GPU, so a cell on N > 1 GPUs runs
+N ranks under torch.distributed.run (z-slab decomposition, NCCL halo
+exchange), each timing its loop, the MAX over ranks reported.  Tables can
+also be assembled from `bench.py --gpus N` lines with `scaling_records`.
 
     python -m paper_1610_09146_b200.benchtables --grids 64,128 \
         --iterations 100 --out results/
@@ -20,6 +23,9 @@ import argparse
 import json
 import math
 import os
+import socket
+import subprocess
+import sys
 from dataclasses import dataclass
 
 import numpy as np
@@ -55,9 +61,11 @@ class TimingRecord:
 
 
 def _time_cell(npoints, plan_name, iterations, constants, warmup=2,
-               repeats=1, dt=None) -> TimingRecord:
+               repeats=1, dt=None, slab=None) -> TimingRecord:
+    """bench.py:51-71 on this process's GPU; with `slab`, this rank's share
+    of a z-slab decomposed grid (the caller reduces over ranks)."""
     import paper_1610_09146_b200 as fd
-    grid = fd.make_grid(npoints, (TWO_PI,) * 3)
+    grid = fd.make_grid(npoints, (TWO_PI,) * 3, slab=slab)
     dt = auto_dt(npoints) if dt is None else dt
     scheme = fd.RKScheme(dt=dt)
     best, final_ke = None, float("nan")
@@ -70,8 +78,70 @@ def _time_cell(npoints, plan_name, iterations, constants, warmup=2,
         if best is None or report.loop_seconds < best:
             best = report.loop_seconds
         final_ke = fd.kinetic_energy_integral(state, grid, rho0)
-    return TimingRecord(tuple(npoints), plan_name, 1, iterations, best,
+    gpus = 1 if slab is None else slab.nranks
+    return TimingRecord(tuple(npoints), plan_name, gpus, iterations, best,
                         final_ke)
+
+
+def _free_port() -> int:
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    return port
+
+
+def time_cell_gpus(npoints, plan_name, gpus, iterations, constants=None,
+                   repeats=1, dt=None) -> TimingRecord:
+    """One timing cell on `gpus` GPUs of this node: in process for one GPU,
+    else `gpus` ranks under torch.distributed.run (127.0.0.1 rendezvous)
+    running `_cell_worker`; loop_seconds is the MAX over ranks."""
+    if gpus == 1:
+        import paper_1610_09146_b200 as fd
+        return _time_cell(npoints, plan_name, iterations,
+                          constants or fd.PhysicalConstants(),
+                          repeats=repeats, dt=dt)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", "-m", __name__, "--cell",
+           "--cell-grid", ",".join(map(str, npoints)), "--cell-plan",
+           plan_name, "--iterations", str(iterations), "--repeats",
+           str(repeats)] + (["--cell-dt", repr(dt)] if dt is not None else [])
+    out = subprocess.run(cmd, capture_output=True, text=True,
+                         cwd=os.path.dirname(os.path.dirname(
+                             os.path.abspath(__file__))))
+    if out.returncode != 0:
+        raise RuntimeError(f"scaling cell on {gpus} GPUs failed:\n"
+                           + out.stderr[-2000:])
+    rec = json.loads([l for l in out.stdout.splitlines()
+                      if l.startswith("{")][-1])
+    return TimingRecord(tuple(rec["grid"]), rec["plan"], rec["workers"],
+                        rec["iterations"], rec["loop_seconds"],
+                        rec["final_ke"])
+
+
+def _cell_worker(a) -> None:
+    """One rank of a multi-GPU cell (launched by time_cell_gpus)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1610_09146_b200 as fd
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    npoints = tuple(int(x) for x in a.cell_grid.split(","))
+    slab = fd.Slab.from_process_group(npoints[0])
+    rec = _time_cell(npoints, a.cell_plan, a.iterations,
+                     fd.PhysicalConstants(), repeats=a.repeats,
+                     dt=a.cell_dt, slab=slab)
+    t = torch.tensor([rec.loop_seconds], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if dist.get_rank() == 0:
+        print(json.dumps({"grid": list(rec.grid), "plan": rec.plan,
+                          "workers": rec.workers,
+                          "iterations": rec.iterations,
+                          "loop_seconds": float(t[0]),
+                          "final_ke": rec.final_ke}), flush=True)
+    dist.destroy_process_group()
 
 
 def bench_variants(grids, plans=("BL", "RA", "RS", "SN", "SS"),
@@ -162,6 +232,64 @@ def scaling_records(lines, strong=True):
     return out
 
 
+def decompose_workers(workers: int) -> tuple:
+    """Split a GPU count into three near-equal grid scale factors
+    (bench.py:160-173): its prime factors, largest first, each multiplied
+    into the currently smallest factor; returned in descending order."""
+    factors = [1, 1, 1]
+    w, d, primes = workers, 2, []
+    while w > 1:
+        while w % d == 0:
+            primes.append(d)
+            w //= d
+        d += 1
+    for p in sorted(primes, reverse=True):
+        factors[int(np.argmin(factors))] *= p
+    return tuple(sorted(factors, reverse=True))
+
+
+def strong_scaling(npoints, plan_name, worker_list, iterations,
+                   constants=None, repeats=1, verbose=False,
+                   timer=time_cell_gpus):
+    """Fixed global grid, varying GPU counts (bench.py:138-157): loop times
+    normalised by the first count's, with the ideal base/N."""
+    raw = []
+    for gpus in worker_list:
+        rec = timer(tuple(npoints), plan_name, gpus, iterations,
+                    constants=constants, repeats=repeats)
+        raw.append(rec)
+        if verbose:
+            print(f"strong {tuple(npoints)} gpus={gpus} "
+                  f"{rec.loop_seconds:.3f}s", flush=True)
+    base_w, base_t = worker_list[0], raw[0].loop_seconds
+    return [ScalingRecord(workers=w, grid=r.grid, loop_seconds=r.loop_seconds,
+                          normalized=r.loop_seconds / base_t,
+                          ideal=base_w / w)
+            for w, r in zip(worker_list, raw)]
+
+
+def weak_scaling(points_per_worker, plan_name, worker_list, iterations,
+                 constants=None, repeats=1, verbose=False,
+                 timer=time_cell_gpus):
+    """Fixed share per GPU (bench.py:176-196): the global grid is the
+    per-GPU grid times decompose_workers(N) axis by axis (the z-slab split
+    then hands each rank the same number of points); ideal 1."""
+    raw = []
+    for gpus in worker_list:
+        f = decompose_workers(gpus)
+        npoints = tuple(points_per_worker[a] * f[a] for a in range(3))
+        rec = timer(npoints, plan_name, gpus, iterations,
+                    constants=constants, repeats=repeats)
+        raw.append(rec)
+        if verbose:
+            print(f"weak {npoints} gpus={gpus} {rec.loop_seconds:.3f}s",
+                  flush=True)
+    base_t = raw[0].loop_seconds
+    return [ScalingRecord(workers=w, grid=r.grid, loop_seconds=r.loop_seconds,
+                          normalized=r.loop_seconds / base_t, ideal=1.0)
+            for w, r in zip(worker_list, raw)]
+
+
 def write_scaling_csv(records, path):
     """bench.py:199-205."""
     with open(path, "w", newline="") as fh:
@@ -179,7 +307,27 @@ def main():
     ap.add_argument("--iterations", type=int, default=100)
     ap.add_argument("--repeats", type=int, default=1)
     ap.add_argument("--out", default=".")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default=None,
+                    help="write scaling.csv over --gpus-list instead")
+    ap.add_argument("--gpus-list", default="1,2,4,8")
+    ap.add_argument("--cell", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--cell-grid", help=argparse.SUPPRESS)
+    ap.add_argument("--cell-plan", help=argparse.SUPPRESS)
+    ap.add_argument("--cell-dt", type=float, default=None,
+                    help=argparse.SUPPRESS)
     a = ap.parse_args()
+    if a.cell:
+        return _cell_worker(a)
+    if a.scaling:
+        n = int(a.grids.split(",")[0])
+        gl = [int(x) for x in a.gpus_list.split(",")]
+        plan = a.plans.split(",")[0]
+        fn = strong_scaling if a.scaling == "strong" else weak_scaling
+        recs = fn((n,) * 3, plan, gl, a.iterations, repeats=a.repeats,
+                  verbose=True)
+        os.makedirs(a.out, exist_ok=True)
+        write_scaling_csv(recs, os.path.join(a.out, "scaling.csv"))
+        return None
     grids = [(int(n),) * 3 for n in a.grids.split(",")]
     recs = bench_variants(grids, a.plans.split(","), a.iterations,
                           repeats=a.repeats, verbose=True)

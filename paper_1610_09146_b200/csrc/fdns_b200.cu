@@ -109,8 +109,9 @@ __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.launch_dependents;");
 }
 
-__global__ void k_primitives(double* __restrict__ F, Coef k, int64_t fs) {
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < fs;
+__global__ void k_primitives(double* __restrict__ F, Coef k, int64_t fs, int64_t c0,
+                             int64_t c1) {
+  for (int64_t c = c0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < c1;
        c += (int64_t)gridDim.x * blockDim.x) {
     double q[5], pr[5];
 #pragma unroll
@@ -1118,7 +1119,22 @@ int32_t fdns_primitives(double* state, const fdns_problem* pb, void* stream) {
   const Geom g = make_geom(pb);
   const Coef k = make_coef(pb);
   const int blocks = (int)std::min<int64_t>((g.fs + 255) / 256, 148 * 16);
-  k_primitives<<<blocks, 256, 0, (cudaStream_t)stream>>>(state, k, g.fs);
+  k_primitives<<<blocks, 256, 0, (cudaStream_t)stream>>>(state, k, g.fs, 0, g.fs);
+  count();
+  return check_launch("primitives kernel");
+}
+
+int32_t fdns_primitives_planes(double* state, int32_t p_lo, int32_t p_hi, const fdns_problem* pb,
+                               void* stream) {
+  if (int e = validate(pb)) return e;
+  const Geom g = make_geom(pb);
+  if (p_lo < 0 || p_hi > g.n0 + 2 * g.h || p_lo > p_hi)
+    return fail("fdns_primitives_planes: plane range outside the padded bundle");
+  if (p_lo == p_hi) return 0;
+  const Coef k = make_coef(pb);
+  const int64_t c0 = p_lo * g.s0, c1 = p_hi * g.s0;
+  const int blocks = (int)std::min<int64_t>((c1 - c0 + 255) / 256, 148 * 16);
+  k_primitives<<<blocks, 256, 0, (cudaStream_t)stream>>>(state, k, g.fs, c0, c1);
   count();
   return check_launch("primitives kernel");
 }

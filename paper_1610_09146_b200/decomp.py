@@ -63,23 +63,45 @@ class Slab:
     def _peer(self, r: int) -> int:
         return r if self.group is None else dist.get_global_rank(self.group, r)
 
-    def exchange(self, bundle: torch.Tensor, h: int) -> None:
-        """Fill the axis-0 ghost planes of every field of `bundle`
-        (nf, n0+2h, P1, P2) from the neighbouring ranks, in place."""
+    def exchange(self, bundle: torch.Tensor, h: int, nf: int | None = None) -> None:
+        """Fill the axis-0 ghost planes of the first `nf` fields (default all)
+        of `bundle` (nf, n0+2h, P1, P2) from the neighbouring ranks, in
+        place.  Each field's h planes are one contiguous run, so they are
+        sent from and received into the bundle itself: no pack or unpack
+        copies, 4 * nf point-to-point operations in one group."""
         n = self.local_n0
-        send_up = bundle[:, n:n + h].contiguous()      # top interior planes
-        send_dn = bundle[:, h:2 * h].contiguous()      # bottom interior planes
-        recv_lo = torch.empty_like(send_up)
-        recv_hi = torch.empty_like(send_dn)
-        ops = [dist.P2POp(dist.isend, send_up, self._peer(self.up), self.group),
-               dist.P2POp(dist.isend, send_dn, self._peer(self.down), self.group),
-               dist.P2POp(dist.irecv, recv_lo, self._peer(self.down), self.group),
-               dist.P2POp(dist.irecv, recv_hi, self._peer(self.up), self.group)]
+        nf = bundle.shape[0] if nf is None else nf
+        up, dn = self._peer(self.up), self._peer(self.down)
+        ops = []
+        for f in range(nf):
+            fb = bundle[f]
+            ops += [dist.P2POp(dist.isend, fb[n:n + h], up, self.group),       # top planes
+                    dist.P2POp(dist.isend, fb[h:2 * h], dn, self.group),       # bottom planes
+                    dist.P2POp(dist.irecv, fb[0:h], dn, self.group),           # low ghosts
+                    dist.P2POp(dist.irecv, fb[n + h:n + 2 * h], up, self.group)]
         for req in dist.batch_isend_irecv(ops):
             req.wait()
-        bundle[:, 0:h].copy_(recv_lo)
-        bundle[:, n + h:n + 2 * h].copy_(recv_hi)
+
+    def exchange_state(self, bundle: torch.Tensor, h: int, problem) -> None:
+        """The per-stage exchange of a state bundle: only the five
+        conservative fields travel (5 x 2h padded planes per neighbour,
+        SURVEY 8e); u, p, T of the received ghost planes are then formed on
+        this rank by the primitives kernel -- the same expressions the
+        sender's stage kernel evaluated, so the same bits."""
+        self.exchange(bundle, h, nf=5)
+        ghost_primitives(bundle, self.local_n0, h, problem)
 
     def allreduce_sum(self, t: torch.Tensor) -> torch.Tensor:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
+
+
+def ghost_primitives(bundle: torch.Tensor, n: int, h: int, problem) -> None:
+    """Primitives (physics.py:185-202) of the 2h axis-0 ghost planes of a
+    state bundle whose conservative ghosts were just received."""
+    from . import _lib
+    lib = _lib.load()
+    for lo in (0, n + h):
+        _lib.check(lib.fdns_primitives_planes(_lib.ptr(bundle), lo, lo + h,
+                                              problem, _lib.stream_handle()),
+                   "ghost-plane primitives")

@@ -122,6 +122,19 @@ def make_grid(npoints, lengths, halo: int = MIN_HALO, slab=None) -> Grid:
     return Grid(npoints=npoints, delta=delta, halo=halo, slab=slab)
 
 
+def as_grid(grid) -> Grid:
+    """This package's Grid for `grid`, which may be the reference's own
+    `fdns.mesh.Grid` (same npoints/delta/halo attributes; parity mode)."""
+    if isinstance(grid, Grid):
+        return grid
+    npoints = tuple(int(n) for n in grid.npoints)
+    lengths = tuple(n * d for n, d in zip(npoints, grid.delta))
+    g = make_grid(npoints, lengths, halo=int(grid.halo))
+    # keep the caller's spacing bits (n * delta / n may round differently)
+    return Grid(npoints=g.npoints, delta=tuple(float(d) for d in grid.delta),
+                halo=g.halo)
+
+
 def device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 

@@ -15,8 +15,8 @@ from dataclasses import dataclass
 
 import torch
 
-from . import _lib
-from .mesh import Grid, alloc_bundle
+from . import _lib, parity
+from .mesh import Grid, alloc_bundle, as_grid
 from .physics import (ConservativeState, PhysicalConstants, Residual,
                       eval_primitives_fused)
 
@@ -325,6 +325,8 @@ class ResidualEvaluator:
                  plan: KernelPlan | str, spec=None, workers: int = 1):
         if isinstance(plan, str):
             plan = build_plan(plan)
+        check_spec(spec)
+        grid = as_grid(grid)
         self.grid = grid
         self.constants = constants
         self.plan = plan
@@ -334,6 +336,7 @@ class ResidualEvaluator:
         nw = workarray_budget(plan)
         self.work = alloc_bundle(grid, nw) if nw > 0 else None
         self._workspace = None
+        self._twin = None        # parity mode: device twin of a host state
 
     @property
     def work_ptr(self) -> int:
@@ -342,12 +345,39 @@ class ResidualEvaluator:
     def evaluate(self, state: ConservativeState, out: Residual) -> Residual:
         """Primitives, work-array fills and the residual kernel
         (plan.py:394-416).  Requires current conservative halos; writes the
-        interior of `out`."""
+        interior of `out`.  `state`/`out` may also be the reference's numpy
+        objects (parity mode, `parity.py`): copied in and out around the
+        device path, with the reference's side effects."""
+        if parity.is_host_state(state) or parity.is_host_residual(out):
+            return self._evaluate_host(state, out)
         eval_primitives_fused(state, self.constants)
         _lib.check(self.lib.fdns_residual(
             self.plan.variant_id, _lib.ptr(state.bundle), self.work_ptr,
             _lib.ptr(out.bundle), self.problem, _lib.stream_handle()),
             f"residual ({self.plan.name})")
+        return out
+
+    def twin(self):
+        """Device state + residual that stand in for host objects."""
+        if self._twin is None:
+            self._twin = (ConservativeState(self.grid), Residual(self.grid))
+        return self._twin
+
+    def _evaluate_host(self, state, out):
+        dev_state, dev_out = self.twin()
+        if parity.is_host_state(state):
+            parity.upload_conservative(state, dev_state)
+        elif isinstance(state, ConservativeState):
+            dev_state.bundle[:5].copy_(state.bundle[:5])
+        else:
+            raise TypeError("evaluate: state must be a ConservativeState or "
+                            "expose field_arrays() of ten numpy arrays")
+        self.evaluate(dev_state, dev_out)
+        if parity.is_host_state(state):
+            parity.download_primitives(dev_state.bundle, state)
+        else:
+            state.bundle[5:].copy_(dev_state.bundle[5:])
+        parity.write_residual(dev_out, out)
         return out
 
     def workspace(self):
@@ -413,7 +443,7 @@ class ResidualEvaluator:
         n = self.grid.local_npoints[0]
         if n < 2 * h:
             self.stage(inp, saved, out, coef)
-            slab.exchange(out, h)
+            slab.exchange_state(out, h, self.problem)
             return
         main = torch.cuda.current_stream()
         if getattr(self, "_comm", None) is None:
@@ -421,7 +451,7 @@ class ResidualEvaluator:
         self.stage_boundary(inp, saved, out, coef)
         self._comm.wait_stream(main)
         with torch.cuda.stream(self._comm):
-            slab.exchange(out, h)
+            slab.exchange_state(out, h, self.problem)
         self.stage_interior(inp, saved, out, coef)
         main.wait_stream(self._comm)
 
@@ -429,10 +459,35 @@ class ResidualEvaluator:
 def assemble_residual(state: ConservativeState, constants: PhysicalConstants,
                       plan: KernelPlan | str, spec=None,
                       workers: int = 1) -> Residual:
-    """One-shot residual assembly (plan.py:419-426)."""
+    """One-shot residual assembly (plan.py:419-426); a reference-style host
+    state gets a numpy residual back (parity mode)."""
     ev = ResidualEvaluator(state.grid, constants, plan, spec, workers)
-    out = Residual(state.grid)
+    out = (parity.HostResidual(ev.grid) if parity.is_host_state(state)
+           else Residual(state.grid))
     return ev.evaluate(state, out)
+
+
+def check_spec(spec) -> None:
+    """The kernels are compiled for the reference's default term list
+    (terms.build_residual_spec(), energy_phi="internal", terms.py:135-200).
+    Accept None, that spec, or any registry with the same 60 derivatives
+    whose `rhoe` is the internal energy; anything else (e.g. the
+    energy_phi="total" list) raises instead of being silently ignored."""
+    if spec is None:
+        return
+    from .terms import DEFAULT_SPEC, RHOE_INTERNAL
+    if spec is DEFAULT_SPEC:
+        return
+    derivs = getattr(spec, "derivatives", None)
+    if not isinstance(derivs, dict) or set(derivs) != set(derivative_ids()):
+        raise NotImplementedError(
+            "spec: the device kernels implement the reference's default "
+            "term list only (60 derivatives, terms.py:135-200)")
+    rhoe = getattr(derivs.get("D(rhoe,x0)"), "expr", None)
+    if rhoe != RHOE_INTERNAL:
+        raise NotImplementedError(
+            "spec: the device kernels implement energy_phi='internal' only "
+            f"(rhoe = {RHOE_INTERNAL}); got rhoe = {rhoe!r}")
 
 
 # The reference's product scratch array name (plan.py:37).  The device fill

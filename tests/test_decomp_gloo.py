@@ -39,6 +39,14 @@ def _worker(rank, world, port, n0, n1, n2, h, q):
         slab.exchange(t, h)
         got = t.numpy()
         ok = np.array_equal(got, want[:, lo:lo + n + 2 * h])
+        # the per-stage exchange sends only the first nf fields (the five
+        # conservative ones of a state): the others' ghosts stay untouched
+        part = np.zeros_like(local)
+        part[:, h:h + n] = want[:, h + lo:h + lo + n]
+        tp = torch.from_numpy(part)
+        slab.exchange(tp, h, nf=2)
+        ok = ok and np.array_equal(tp.numpy()[:2], want[:2, lo:lo + n + 2 * h])
+        ok = ok and not tp.numpy()[2, :h].any() and not tp.numpy()[2, n + h:].any()
         # allreduce helper
         s = slab.allreduce_sum(torch.tensor([float(rank + 1)]))
         q.put((rank, ok, float(s[0])))

@@ -545,8 +545,10 @@ def test_slab_decomposition_bitwise_invariant(kernel_path, variant, nranks, spli
             dn, up = slabs[r - 1], slabs[(r + 1) % nranks]
             b, bd, bu = bundles[r], bundles[r - 1], bundles[(r + 1) % nranks]
             n = sl.local_n0
-            b[:, 0:h].copy_(bd[:, dn.local_n0:dn.local_n0 + h])
-            b[:, n + h:n + 2 * h].copy_(bu[:, h:2 * h])
+            b[:5, 0:h].copy_(bd[:5, dn.local_n0:dn.local_n0 + h])
+            b[:5, n + h:n + 2 * h].copy_(bu[:5, h:2 * h])
+            # what Slab.exchange_state does after receiving the 5 fields
+            fd.decomp.ghost_primitives(b, n, h, evs[r].problem)
 
     for _ in range(2):
         X = [st.bundle for st in states]
@@ -592,8 +594,10 @@ def _emulated_slab_run(variant, X0, npts, nranks, steps, dt, split=True):
             dn = slabs[r - 1]
             b, bd, bu = bundles[r], bundles[r - 1], bundles[(r + 1) % nranks]
             n = sl.local_n0
-            b[:, 0:h].copy_(bd[:, dn.local_n0:dn.local_n0 + h])
-            b[:, n + h:n + 2 * h].copy_(bu[:, h:2 * h])
+            b[:5, 0:h].copy_(bd[:5, dn.local_n0:dn.local_n0 + h])
+            b[:5, n + h:n + 2 * h].copy_(bu[:5, h:2 * h])
+            # what Slab.exchange_state does after receiving the 5 fields
+            fd.decomp.ghost_primitives(b, n, h, evs[r].problem)
 
     scheme = fd.RKScheme(dt=dt)
     for _ in range(steps):

@@ -249,3 +249,59 @@ def test_terms_registry_matches_reference_goldens(golden_meta):
     assert fd.plan.DEFAULT_SPEC.occurrences == spec.occurrences
     with pytest.raises(ValueError):
         fd.terms.build_residual_spec("total")
+
+
+def test_spec_check_rejects_other_term_lists():
+    """ResidualEvaluator(spec=...) no longer ignores spec: the default term
+    list passes, anything else raises (plan.check_spec)."""
+    from dataclasses import dataclass, field
+    fplan.check_spec(None)
+    fplan.check_spec(fd.terms.DEFAULT_SPEC)
+    fplan.check_spec(fd.terms.build_residual_spec())
+
+    @dataclass
+    class D:
+        expr: str
+
+    @dataclass
+    class Spec:
+        derivatives: dict = field(default_factory=dict)
+
+    ok = Spec({d: D("x") for d in fplan.derivative_ids()})
+    ok.derivatives["D(rhoe,x0)"] = D(fd.terms.RHOE_INTERNAL)
+    fplan.check_spec(ok)                          # a reference-built default spec
+    total = Spec({d: D("x") for d in fplan.derivative_ids()})
+    total.derivatives["D(rhoe,x0)"] = D("rhoE")   # energy_phi="total"
+    with pytest.raises(NotImplementedError):
+        fplan.check_spec(total)
+    with pytest.raises(NotImplementedError):
+        fplan.check_spec(Spec({"D(rho,x0)": D("rho")}))
+    with pytest.raises(ValueError):
+        fd.terms.build_residual_spec("total")
+
+
+def test_decompose_workers_and_scaling_drivers():
+    """decompose_workers (bench.py:160-173 semantics) and the strong/weak
+    drivers' normalisation, with a stand-in timer (no GPU)."""
+    from paper_1610_09146_b200 import benchtables as bt
+    assert bt.decompose_workers(1) == (1, 1, 1)
+    assert bt.decompose_workers(2) == (2, 1, 1)
+    assert bt.decompose_workers(4) == (2, 2, 1)
+    assert bt.decompose_workers(8) == (2, 2, 2)
+    assert bt.decompose_workers(12) == (3, 2, 2)
+    assert bt.decompose_workers(6) == (3, 2, 1)
+    calls = []
+
+    def timer(npoints, plan, gpus, iterations, constants=None, repeats=1):
+        calls.append((npoints, gpus))
+        sec = float(np.prod(npoints)) / gpus * 1e-6   # perfect scaling
+        return bt.TimingRecord(tuple(npoints), plan, gpus, iterations, sec)
+
+    st = bt.strong_scaling((64, 64, 64), "SS", [1, 2, 4, 8], 10, timer=timer)
+    assert [r.ideal for r in st] == [1.0, 0.5, 0.25, 0.125]
+    assert [r.normalized for r in st] == pytest.approx([1, 0.5, 0.25, 0.125])
+    wk = bt.weak_scaling((32, 32, 32), "SN", [1, 2, 4, 8], 10, timer=timer)
+    assert [r.grid for r in wk] == [(32, 32, 32), (64, 32, 32),
+                                    (64, 64, 32), (64, 64, 64)]
+    assert all(r.ideal == 1.0 for r in wk)
+    assert [r.normalized for r in wk] == pytest.approx([1, 1, 1, 1])
