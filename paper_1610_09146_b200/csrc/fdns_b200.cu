@@ -252,6 +252,9 @@ __device__ __forceinline__ void fill_axis_all(const Coef& k, const GAcc& a,
 // All 54 plain/product derivatives of an interior point in one pass over the
 // fields (the reference's separate fill loops, plan.py:369-392, fused; each
 // value is the same expression, so bitwise equal).
+// AXES: bit a = fill the 18 slots of axis a (7 = all 54; 6 = the in-plane
+// 36, beside the axis-0-marching k_fill_bl_ax0).
+template <int AXES = 7>
 __global__ void __launch_bounds__(256) k_fill_bl_all(const double* __restrict__ in,
                                                      double* __restrict__ wa, Coef k, Geom g) {
   pdl_entry();
@@ -261,9 +264,221 @@ __global__ void __launch_bounds__(256) k_fill_bl_all(const double* __restrict__ 
   if (kk < 0 || kk >= g.n2 || jj >= g.n1) return;
   const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + (kk + g.h);
   GAcc a{in, c, g.s0, g.s1, g.fs};
-  fill_axis_all<0, 0>(k, a, wa, g.fs);
-  fill_axis_all<1, 0>(k, a, wa, g.fs);
-  fill_axis_all<2, 0>(k, a, wa, g.fs);
+  if constexpr (AXES & 1) fill_axis_all<0, 0>(k, a, wa, g.fs);
+  if constexpr (AXES & 2) fill_axis_all<1, 0>(k, a, wa, g.fs);
+  if constexpr (AXES & 4) fill_axis_all<2, 0>(k, a, wa, g.fs);
+}
+
+// ---------------------------------------------------------------------------
+// Axis-0-marching fills.  A thread owns one (axis-1, axis-2) column and walks
+// NPL consecutive planes, keeping the five-plane axis-0 stencil window of the
+// fields it differentiates along axis 0 in registers (QAcc): each input
+// value comes from DRAM about once (plus 4/NPL halo planes per chunk)
+// instead of once per axis-0 tap -- with 54 output streams flowing through
+// L2, the one-thread-per-point fill re-read every input ~5x (ncu at 512^3:
+// 55 GB of reads for 10.7 GB of inputs).  In-plane taps still come through
+// the read-only path (L1/L2 hits: the CTA's neighbouring columns loaded
+// them).  Same expressions through the same eval_slot/d1 templates, so the
+// bits are the point kernel's.
+// ---------------------------------------------------------------------------
+template <int NQ>
+struct QAcc {
+  static constexpr bool kInternalEnergy = false;
+  const double (&q)[NQ][5];   // q[f][d]: field f at axis-0 offset d-2
+  const double* __restrict__ b;
+  int64_t c, s0, s1, fs;
+  __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
+    if (dj == 0 && dk == 0) return q[f][di + 2];
+    return __ldg(b + f * fs + c + di * s0 + dj * s1 + dk);
+  }
+};
+
+template <int NQ>
+__device__ __forceinline__ void load_plane(double (&dst)[NQ], const double* __restrict__ in,
+                                           int64_t c, int64_t fs, const int (&fld)[NQ]) {
+#pragma unroll
+  for (int f = 0; f < NQ; ++f) dst[f] = __ldg(in + fld[f] * fs + c);
+}
+
+template <int A_, int L, int NQ>
+__device__ __forceinline__ void fill_axis_q(const Coef& k, const QAcc<NQ>& a,
+                                            double* __restrict__ wa, int64_t fs) {
+  wa[slot(A_, L) * fs + a.c] = eval_slot<A_, L>(k, a);
+  if constexpr (L + 1 < S_PER_AXIS) fill_axis_q<A_, L + 1>(k, a, wa, fs);
+}
+
+// BL: all 54 plain/product derivatives (the 10 point fields queued).
+constexpr int MARCH_BX = 32, MARCH_BY = 4;
+#ifndef FDNS_MARCH_MINB
+#define FDNS_MARCH_MINB 1
+#endif
+template <int NPL, int AXES = 7>
+__global__ void __launch_bounds__(MARCH_BX * MARCH_BY, FDNS_MARCH_MINB) k_fill_bl_march(
+    const double* __restrict__ in, double* __restrict__ wa, Coef k, Geom g) {
+  pdl_entry();
+  const int kk = point_k(g);
+  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
+  if (kk < 0 || kk >= g.n2 || jj >= g.n1) return;
+  const int i0 = blockIdx.z * NPL, i1 = min(i0 + NPL, g.n0);
+  const int64_t col = (int64_t)(jj + g.h) * g.s1 + (kk + g.h);
+  constexpr int fld[NFIELDS] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9};
+  double q[NFIELDS][5], nx[NFIELDS];
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    double t[NFIELDS];
+    load_plane<NFIELDS>(t, in, (int64_t)(i0 - 2 + d + g.h) * g.s0 + col, g.fs, fld);
+#pragma unroll
+    for (int f = 0; f < NFIELDS; ++f) q[f][d] = t[f];
+  }
+  load_plane<NFIELDS>(nx, in, (int64_t)(i0 + 2 + g.h) * g.s0 + col, g.fs, fld);
+#pragma unroll 1
+  for (int i = i0; i < i1; ++i) {
+#pragma unroll
+    for (int f = 0; f < NFIELDS; ++f) q[f][4] = nx[f];
+    if (i + 1 < i1)   // next step's new plane, loaded under this step's work
+      load_plane<NFIELDS>(nx, in, (int64_t)(i + 3 + g.h) * g.s0 + col, g.fs, fld);
+    const QAcc<NFIELDS> a{q, in, (int64_t)(i + g.h) * g.s0 + col, g.s0, g.s1, g.fs};
+    if constexpr (AXES & 1) fill_axis_q<0, 0>(k, a, wa, g.fs);
+    if constexpr (AXES & 2) fill_axis_q<1, 0>(k, a, wa, g.fs);
+    if constexpr (AXES & 4) fill_axis_q<2, 0>(k, a, wa, g.fs);
+#pragma unroll
+    for (int f = 0; f < NFIELDS; ++f)
+#pragma unroll
+      for (int d = 0; d < 4; ++d) q[f][d] = q[f][d + 1];
+  }
+}
+
+// The same with the axis-0 window in shared memory instead of registers:
+// each thread keeps its own column's ten fields on five planes in a ring
+// (slot = plane mod 5, [slot][field][thread]: consecutive threads hit
+// consecutive words), so no barrier is needed and the registers are left to
+// the in-plane taps -- four 128-thread CTAs per SM instead of the two the
+// 255-register queue allowed (ncu at 512^3: 12% warps active, long-
+// scoreboard bound, 4.2 TB/s).
+struct SQAcc {
+  static constexpr bool kInternalEnergy = false;
+  const double* p[5];          // plane slots of axis-0 offsets -2..+2 (this thread)
+  const double* __restrict__ b;
+  int64_t c, s0, s1, fs;
+  __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
+    if (dj == 0 && dk == 0) return p[di + 2][f * (MARCH_BX * MARCH_BY)];
+    return __ldg(b + f * fs + c + di * s0 + dj * s1 + dk);
+  }
+};
+
+template <int A_, int L>
+__device__ __forceinline__ void fill_axis_sq(const Coef& k, const SQAcc& a,
+                                             double* __restrict__ wa, int64_t fs) {
+  wa[slot(A_, L) * fs + a.c] = eval_slot<A_, L>(k, a);
+  if constexpr (L + 1 < S_PER_AXIS) fill_axis_sq<A_, L + 1>(k, a, wa, fs);
+}
+
+#ifndef FDNS_MARCH_SMEM_MINB
+#define FDNS_MARCH_SMEM_MINB 3
+#endif
+constexpr int MARCH_NT = MARCH_BX * MARCH_BY;
+constexpr int MARCH_SMEM = 5 * NFIELDS * MARCH_NT * 8;   // 51200 B
+template <int NPL>
+__global__ void __launch_bounds__(MARCH_NT, FDNS_MARCH_SMEM_MINB) k_fill_bl_march_s(
+    const double* __restrict__ in, double* __restrict__ wa, Coef k, Geom g) {
+  extern __shared__ __align__(16) double qs[];
+  pdl_entry();
+  const int kk = point_k(g);
+  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
+  if (kk < 0 || kk >= g.n2 || jj >= g.n1) return;
+  const int tid = threadIdx.y * MARCH_BX + threadIdx.x;
+  double* mine = qs + tid;
+  auto slot_ptr = [&](int plane) { return mine + (plane % 5) * NFIELDS * MARCH_NT; };
+  const int i0 = blockIdx.z * NPL, i1 = min(i0 + NPL, g.n0);
+  const int64_t col = (int64_t)(jj + g.h) * g.s1 + (kk + g.h);
+  // planes i0-2 .. i0+1 (index shifted by +2 so it stays non-negative)
+#pragma unroll 1
+  for (int d = 0; d < 4; ++d) {
+    double* sp = slot_ptr(i0 + d);
+    const int64_t c = (int64_t)(i0 - 2 + d + g.h) * g.s0 + col;
+#pragma unroll
+    for (int f = 0; f < NFIELDS; ++f) sp[f * MARCH_NT] = __ldg(in + f * g.fs + c);
+  }
+  double nx[NFIELDS];
+#pragma unroll
+  for (int f = 0; f < NFIELDS; ++f)
+    nx[f] = __ldg(in + f * g.fs + (int64_t)(i0 + 2 + g.h) * g.s0 + col);
+#pragma unroll 1
+  for (int i = i0; i < i1; ++i) {
+    {
+      double* sp = slot_ptr(i + 4);   // plane i+2 (offset +2)
+#pragma unroll
+      for (int f = 0; f < NFIELDS; ++f) sp[f * MARCH_NT] = nx[f];
+    }
+    if (i + 1 < i1) {
+#pragma unroll
+      for (int f = 0; f < NFIELDS; ++f)
+        nx[f] = __ldg(in + f * g.fs + (int64_t)(i + 3 + g.h) * g.s0 + col);
+    }
+    SQAcc a;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) a.p[d] = slot_ptr(i + d);
+    a.b = in;
+    a.c = (int64_t)(i + g.h) * g.s0 + col;
+    a.s0 = g.s0; a.s1 = g.s1; a.fs = g.fs;
+    fill_axis_sq<0, 0>(k, a, wa, g.fs);
+    fill_axis_sq<1, 0>(k, a, wa, g.fs);
+    fill_axis_sq<2, 0>(k, a, wa, g.fs);
+  }
+}
+
+// SS/RS: the nine velocity gradients (u0..u2 queued; queue slot q = field
+// U0 + q, remapped by QAccU below).
+struct QAccU {   // (E_FIELD taps only: no kInternalEnergy needed)
+  const double (&q)[3][5];
+  const double* __restrict__ b;
+  int64_t c, s0, s1, fs;
+  __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
+    if (dj == 0 && dk == 0) return q[f - U0][di + 2];
+    return __ldg(b + f * fs + c + di * s0 + dj * s1 + dk);
+  }
+};
+
+template <int NPL>
+__global__ void __launch_bounds__(MARCH_BX * MARCH_BY) k_grad_ss_march(
+    const double* __restrict__ in, double* __restrict__ ws, Coef k, Geom g) {
+  pdl_entry();
+  const int kk = point_k(g);
+  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
+  if (kk < 0 || kk >= g.n2 || jj >= g.n1) return;
+  const int i0 = blockIdx.z * NPL, i1 = min(i0 + NPL, g.n0);
+  const int64_t col = (int64_t)(jj + g.h) * g.s1 + (kk + g.h);
+  constexpr int fld[3] = {U0, U1, U2};
+  double q[3][5], nx[3];
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    double t[3];
+    load_plane<3>(t, in, (int64_t)(i0 - 2 + d + g.h) * g.s0 + col, g.fs, fld);
+#pragma unroll
+    for (int f = 0; f < 3; ++f) q[f][d] = t[f];
+  }
+  load_plane<3>(nx, in, (int64_t)(i0 + 2 + g.h) * g.s0 + col, g.fs, fld);
+#pragma unroll 1
+  for (int i = i0; i < i1; ++i) {
+#pragma unroll
+    for (int f = 0; f < 3; ++f) q[f][4] = nx[f];
+    if (i + 1 < i1) load_plane<3>(nx, in, (int64_t)(i + 3 + g.h) * g.s0 + col, g.fs, fld);
+    const int64_t c = (int64_t)(i + g.h) * g.s0 + col;
+    const QAccU a{q, in, c, g.s0, g.s1, g.fs};
+    ws[(0 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U0, 0>(k, a);
+    ws[(0 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U0, 0>(k, a);
+    ws[(0 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U0, 0>(k, a);
+    ws[(1 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U1, 0>(k, a);
+    ws[(1 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U1, 0>(k, a);
+    ws[(1 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U1, 0>(k, a);
+    ws[(2 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U2, 0>(k, a);
+    ws[(2 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U2, 0>(k, a);
+    ws[(2 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U2, 0>(k, a);
+#pragma unroll
+    for (int f = 0; f < 3; ++f)
+#pragma unroll
+      for (int d = 0; d < 4; ++d) q[f][d] = q[f][d + 1];
+  }
 }
 
 // D(u_Q, x_Q) on the ghost frame only: points whose axis-Q coordinate is
@@ -992,6 +1207,26 @@ int launch_residual(int variant, const double* in, const double* saved, double* 
   return check_launch("residual kernel");
 }
 
+// Planes per thread of the axis-0-marching fills; FDNS_MARCH_FILL=0 turns
+// them off (A/B).
+#ifndef FDNS_MARCH_NPL
+#define FDNS_MARCH_NPL 32
+#endif
+constexpr int MARCH_NPL = FDNS_MARCH_NPL;
+// BL fill: 0 = point kernel, 1 = register-queue march, 2 = shared-memory
+// queue march, 3 = axis-0 march + in-plane point kernel; -1 (default) = 2
+// on large planes, else 0.  Whole BL RK3 steps (tools/step_timing.py,
+// profiles/r02_bl_fill_ab.txt): 512^3 point 109.2 ms, 1: 102.6, 2: 100.6,
+// 3: 102.4; 256^3 point 12.8 ms, 2: 13.1.  The write-dominated fill runs
+// at ~4.2-4.8 TB/s whichever way (HBM read/write turnaround: the read-heavy
+// BL residual streams 6.4 TB/s); the marching fills cut its reads from 55
+// to 15 GB per launch at 512^3.
+const int g_march_fill = std::getenv("FDNS_MARCH_FILL") ? std::atoi(std::getenv("FDNS_MARCH_FILL")) : -1;
+inline int march_fill_mode(const Geom& g) {
+  if (g_march_fill >= 0) return g_march_fill;
+  return (int64_t)g.n1 * g.n2 >= 384 * 384 ? 2 : 0;
+}
+const bool g_march_ss = std::getenv("FDNS_MARCH_SS") && std::atoi(std::getenv("FDNS_MARCH_SS")) == 1;
 // A/B switch: FDNS_SS_FILL_1D=1 selects the one-launch grid-stride SS fill.
 const bool g_ss_fill_3d = std::getenv("FDNS_SS_FILL_1D") == nullptr;
 
@@ -1013,8 +1248,32 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
     if (pdl) launch_pdl(k_diag_ghost, dim3(nb), dim3(256), 0, s, in, d0, d1p, d2p, k, g, f0, f1, f2);
     else k_diag_ghost<<<nb, 256, 0, s>>>(in, d0, d1p, d2p, k, g, f0, f1, f2);
   };
+  // axis-0-marching fills (FDNS_MARCH_FILL=0 restores the point fills)
+  const dim3 mblk(MARCH_BX, MARCH_BY, 1);
+  auto march_grid = [&](int npl) {
+    dim3 m = point_grid(g, mblk);
+    m.z = (g.n0 + npl - 1) / npl;
+    return m;
+  };
   if (variant == FDNS_BL) {
-    launch_pdl(k_fill_bl_all, grd, blk, 0, s, in, work, k, g);
+    const int mode = march_fill_mode(g);
+    if (mode == 2 && g.n0 >= 2 * MARCH_NPL) {
+      static std::atomic<uint64_t> attr{0};
+      once_per_device(attr, [] {
+        cudaFuncSetAttribute(k_fill_bl_march_s<MARCH_NPL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, MARCH_SMEM);
+      });
+      launch_pdl(k_fill_bl_march_s<MARCH_NPL>, march_grid(MARCH_NPL), mblk, MARCH_SMEM, s, in,
+                 work, k, g);
+    } else if (mode == 3 && g.n0 >= 2 * MARCH_NPL) {
+      // axis 0 by the marching kernel, axes 1-2 by the point kernel
+      launch_pdl(k_fill_bl_march<MARCH_NPL, 1>, march_grid(MARCH_NPL), mblk, 0, s, in, work, k, g);
+      launch_pdl(k_fill_bl_all<6>, grd, blk, 0, s, in, work, k, g);
+      count();
+    } else if (mode == 1 && g.n0 >= 2 * MARCH_NPL)
+      launch_pdl(k_fill_bl_march<MARCH_NPL>, march_grid(MARCH_NPL), mblk, 0, s, in, work, k, g);
+    else
+      launch_pdl(k_fill_bl_all<7>, grd, blk, 0, s, in, work, k, g);
     ghosts(work + slot(0, S_U + 0) * g.fs, work + slot(1, S_U + 1) * g.fs,
            work + slot(2, S_U + 2) * g.fs, true);
     launch_pdl(k_fill_cross, grd, blk, 0, s, work, k, g);
@@ -1025,7 +1284,10 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
   // frames (+6% SS/RS steps at 256^3); below, one grid-stride launch
   // (its single launch wins at 64^3: -4% otherwise)
   if ((variant == FDNS_SS || variant == FDNS_RS) && g_ss_fill_3d && g.n2 >= 128) {
-    k_grad_ss_interior<<<grd, blk, 0, s>>>(in, work, k, g);
+    if (g_march_ss && g.n0 >= 2 * MARCH_NPL)
+      k_grad_ss_march<MARCH_NPL><<<march_grid(MARCH_NPL), mblk, 0, s>>>(in, work, k, g);
+    else
+      k_grad_ss_interior<<<grd, blk, 0, s>>>(in, work, k, g);
     ghosts(work + 0 * g.fs, work + 4 * g.fs, work + 8 * g.fs, false);
     count(2);
     return check_launch("SS fills");

@@ -323,16 +323,37 @@ struct SSProvider {
 // The five residual expressions (terms.py:151-183), left-to-right.
 // Point values: r[10] = rho, rhou0..2, rhoE, u0..2, p, T at the centre.
 // ---------------------------------------------------------------------------
-// Each G/X call site gets a distinct occurrence id (__COUNTER__), salted by
-// the helper's template arguments so that e.g. the three div(u) sums inside
-// tau<0,0>, tau<1,1>, tau<2,2> stay distinct occurrences, as in the
-// reference's expression strings.
+// Occurrence ids of the INLINE providers (RA, RS).  By default every G/X
+// call site gets its own id (__COUNTER__, salted by the helper's template
+// arguments, so e.g. the three div(u) sums inside tau<0,0>, tau<1,1>,
+// tau<2,2> stay distinct): every source occurrence is recomputed.
+//
+// That is more recompute than the reference *executes*: its RA kernel has one
+// numba statement per residual, each ending in a store to an output array
+// that may alias the inputs, so LLVM merges identical loads and operations
+// within a residual statement and never across statements.
+// tools/ref_cse_count.py counts the reference's generated kernels under that
+// rule -- RA 1074, RS 729, SN 774, SS 609, BL 198 FP ops per point -- against
+// the disassembly counts of SURVEY.md 2.1 (RA 1065, SN 750, SS 585, BL 189).
+// FDNS_RA_PER_EQUATION=1 reproduces it (every occurrence carries the id of
+// its residual equation, EQ: 0 mass, 1-3 momentum, 4 energy), but the merged
+// values stay live across the long energy equation: the RA stage kernel
+// then needs 255 registers plus 476 B of spills and ran 1.5x slower at
+// 256^3-512^3 (RS +3-6%), so the per-occurrence form stays the default.
+#ifndef FDNS_RA_PER_EQUATION
+#define FDNS_RA_PER_EQUATION 0
+#endif
+#if FDNS_RA_PER_EQUATION
+#define G(a, L) P.template g<a, L, EQ>()
+#define X(j, o) P.template x<j, o, EQ>()
+#else
 #define G(a, L) P.template g<a, L, __COUNTER__ * 16 + SALT>()
 #define X(j, o) P.template x<j, o, __COUNTER__ * 16 + SALT>()
+#endif
 
 template <int I, class Pv>
 __device__ __forceinline__ double viscous(const Coef& k, const Pv& P) {
-  constexpr int SALT = 1 + I;
+  [[maybe_unused]] constexpr int SALT = 1 + I, EQ = 4;   // used by the energy equation
   // c43*D2(u_i,x_i) + [j != i, ascending: inv_Re*D2(u_i,x_j) + c13*DD(u_j,x_i,x_j)]
   // (terms.py:113-123)
   constexpr int J1 = I == 0 ? 1 : 0;
@@ -347,7 +368,7 @@ __device__ __forceinline__ double viscous(const Coef& k, const Pv& P) {
 // bitwise the full chain).
 template <int I, class Pv>
 __device__ __forceinline__ double momentum_prefix(const Coef& k, const Pv& P, const double* r) {
-  constexpr int SALT = 4 + I;
+  [[maybe_unused]] constexpr int SALT = 4 + I, EQ = 1 + I;
   const double rui = r[RU0 + I];
   const double conv = G(0, S_RUU + I) + r[U0] * G(0, S_RU + I) + rui * G(0, S_U + 0) +
                       G(1, S_RUU + I) + r[U1] * G(1, S_RU + I) + rui * G(1, S_U + 1) +
@@ -357,7 +378,7 @@ __device__ __forceinline__ double momentum_prefix(const Coef& k, const Pv& P, co
 
 template <int I, class Pv>
 __device__ __forceinline__ double momentum_suffix(const Coef& k, const Pv& P, double pre) {
-  constexpr int SALT = 10 + I;
+  [[maybe_unused]] constexpr int SALT = 10 + I, EQ = 1 + I;
   constexpr int J1 = I == 0 ? 1 : 0;
   constexpr int J2 = I == 2 ? 1 : 2;
   return pre + k.c43 * G(I, S_U2 + I) + k.inv_Re * G(J1, S_U2 + I) + k.c13 * X(J1, I) +
@@ -371,7 +392,7 @@ __device__ __forceinline__ double momentum(const Coef& k, const Pv& P, const dou
 
 template <int I, int J, class Pv>
 __device__ __forceinline__ double tau(const Coef& k, const Pv& P) {
-  constexpr int SALT = 7 + I * 3 + J - (I * 3 + J > 8 ? 9 : 0);
+  [[maybe_unused]] constexpr int SALT = 7 + I * 3 + J - (I * 3 + J > 8 ? 9 : 0), EQ = 4;
   // terms.py:126-132
   if constexpr (I == J)
     return 2.0 * k.inv_Re * G(I, S_U + I) - k.c23 * (G(0, S_U + 0) + G(1, S_U + 1) + G(2, S_U + 2));
@@ -382,7 +403,7 @@ __device__ __forceinline__ double tau(const Coef& k, const Pv& P) {
 // mass (terms.py:151-156)
 template <class Pv>
 __device__ __forceinline__ double mass_residual(const Coef& k, const Pv& P, const double* r) {
-  constexpr int SALT = 13;
+  [[maybe_unused]] constexpr int SALT = 13, EQ = 0;
   const double acc = G(0, S_RU + 0) + r[U0] * G(0, S_RHO) + r[RHO] * G(0, S_U + 0) +
                      G(1, S_RU + 1) + r[U1] * G(1, S_RHO) + r[RHO] * G(1, S_U + 1) +
                      G(2, S_RU + 2) + r[U2] * G(2, S_RHO) + r[RHO] * G(2, S_U + 2);
@@ -392,7 +413,7 @@ __device__ __forceinline__ double mass_residual(const Coef& k, const Pv& P, cons
 // energy (terms.py:167-183), split after the nine stress-work terms
 template <bool RHOE_INTERNAL, class Pv>
 __device__ __forceinline__ double energy_prefix(const Coef& k, const Pv& P, const double* r) {
-  constexpr int SALT = 14;
+  [[maybe_unused]] constexpr int SALT = 14, EQ = 4;
   const double rhoe = RHOE_INTERNAL ? r[RHOE_F]
                                     : r[RHOE_F] - 0.5 * (r[RU0] * r[U0] + r[RU1] * r[U1] +
                                                          r[RU2] * r[U2]);
