@@ -50,19 +50,39 @@ DT = {64: 3.385e-3, 128: 1.69e-3, 256: 8.5e-4, 512: 4.2e-4, 32: 2e-3,
 CONFIG_NAMES = {32: "C1", 64: "C2", 128: "C3", 256: "C4", 512: "C5",
                 1024: "C5 (weak counterpart)"}
 
-# Algorithmic per-point costs of one fused stage kernel:
-#   flops F_v = residual source flops + 10 (update) + 13 (primitives)
+# Algorithmic per-point costs of one RK stage ("Whole RK stage
+# per point"):
+#   flops F_v = residual source flops + fills + 10 (update) + 13 (primitives)
+#   (BL 223 + 360 fill + 18 mixed fill + 23 ... as tabulated there)
 #   bytes: model M for the fused stage = read 10 state fields + 5 saved
 #   (stage 0: saved == input) + write 10, plus each FETCH array written and
 #   read once by the fills/residual.
 RESIDUAL_FLOPS = {"BL": 223, "RA": 1318, "RS": 838, "SN": 895, "SS": 730}
-STAGE_FLOPS = {v: f + 23 for v, f in RESIDUAL_FLOPS.items()}
+STAGE_FLOPS = {"BL": 627, "RA": 1341, "RS": 906, "SN": 918, "SS": 798}
 N_WORK = {"BL": 60, "RA": 0, "RS": 9, "SN": 0, "SS": 9}
 
 
+# Algorithmic HBM bytes per point of one RK stage: SURVEY.md 8d's model M
+# (primitives materialised once, each FETCH array written and read once,
+# the residual kernel reading its point fields and the RK update its 15
+# accesses, save-state 10/3), minus the 80 B of the residual store and
+# re-read for a path whose residual and update are fused ("If
+# residual and update are fused ... subtract 10 accesses (80 B)") -- the
+# contract's per-unit figure.
+SURVEY_MODEL_M = {"BL": 1370.7, "RA": 346.7, "RS": 514.7, "SN": 346.7, "SS": 514.7}
+
+
 def stage_bytes(v: str) -> float:
-    """Compulsory HBM bytes per point of one fused stage (avg over the 3
-    stages: stage 0 reads its saved fields as the input)."""
+    """SURVEY 8d model-M bytes per point of one fused RK stage."""
+    return SURVEY_MODEL_M[v] - 80.0
+
+
+def stage_bytes_design(v: str) -> float:
+    """The stricter compulsory bytes of this design's fused stage (round
+    1's model; primitives are never materialised here -- p, T are derived
+    on arrival -- and the save-state copy is gone): read 10 state fields +
+    5 saved (stage 0 reads its saved fields as the input) + write 10, plus
+    each FETCH array written and read once."""
     state = (10 + 5 * 2.0 / 3.0 + 10) * 8.0
     return state + 2 * 8.0 * N_WORK[v]
 
@@ -317,8 +337,9 @@ def bench_variant(fd, variant, grid, cons_host, steps, warmup, flush_buf, lib,
 
 
 def measured_traffic(variant: str, n: int):
-    """DRAM bytes per launch of the headline stage kernel from the committed
-    ncu --set full capture (profiles/traffic.json), if one matches."""
+    """DRAM bytes (read + write) of one RK stage -- all its launches: the
+    fills and the stage kernel -- from the committed ncu --set full capture
+    (profiles/traffic.json, tools/traffic_json.py), if one matches."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(path):
         return None
@@ -328,13 +349,14 @@ def measured_traffic(variant: str, n: int):
     return {"bytes_per_launch": rec["dram_bytes"], "unit": "B",
             "bytes_per_point": rec["dram_bytes"] / n ** 3,
             "fp64_insts_per_point": rec.get("fp64_insts_per_point"),
+            "kernels": rec.get("kernels"),
             "source": rec["source"]}
 
 
 def stage_sweep(fd, lib, sizes, variants, flush, fp64_tf, hbm_peak):
     """Steady-state view: one fused stage per variant at larger grids
     (CUDA events, L2 flushed before each launch).  Informational; the
-    headline is the configs[1] workload above."""
+    headline is the C5 workload above."""
     import torch
     from paper_1610_09146_b200 import _lib
     c = fd.PhysicalConstants()
@@ -465,6 +487,18 @@ def variant_roofline(v, rec, fp64_tf, hbm_peak, hbm_src, n):
                 "peak": hbm_peak, "unit": "GB/s",
                 "peak_source": f"{hbm_src} (MEASURED_PEAKS.json hbm_gbs)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["bytes_model"] = ("SURVEY 8d model M, fused residual+update "
+                           f"(-80 B): {stage_bytes(v):.1f} B/pt; flops F_v "
+                           f"{STAGE_FLOPS[v]}/pt")
+    # the stricter design-compulsory byte model (round 1's): same time, the
+    # roofline min(FP64, HBM) recomputed with it
+    tb = stage_bytes_design(v) / (hbm_peak * 1e9)
+    tf = STAGE_FLOPS[v] / (fp64_tf * 1e12)
+    pts_s = rec["local_pts"] / (rec["stage_kernel_ms"] / 1e3)
+    roof["design_compulsory_view"] = {
+        "bytes_per_pt": stage_bytes_design(v),
+        "bound": "fp64" if tf >= tb else "hbm",
+        "frac": pts_s * max(tf, tb)}
     tr = measured_traffic(v, n)
     roof["traffic"] = tr["bytes_per_launch"] if tr else None
     roof["traffic_detail"] = tr
@@ -558,6 +592,10 @@ def main_ours(args):
     e2e = bench_e2e(fd, head, grid, cons_host, max(3, min(args.steps,
                                                           args.e2e_steps)))
     if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
         return
     roof = dict(r["roofline"])
 
@@ -601,6 +639,7 @@ def main_ours(args):
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
+        dist.barrier()
         dist.destroy_process_group()
 
 
