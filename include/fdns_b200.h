@@ -117,10 +117,10 @@ int32_t fdns_stage_planes(int32_t variant, const double* in,
                           const fdns_problem* pb, void* stream);
 
 /* Test hook selecting the kernel family: 0 = default (TMA-staged tiled
- * kernels where the row pitch allows; SN on the 12-warp kernel where its
- * tile rows fit the grid), 1 = one-thread-per-point kernels (global-memory
- * taps) for every variant; SN only: 2 = the 8-warp tiled kernel,
- * 4 = eagerly evaluated derivatives, 5 = the 12-warp kernel.  All paths are
+ * kernels where the row pitch allows), 1 = one-thread-per-point kernels (global-memory
+ * taps) for every variant; 2 = the 8-warp tiled kernel (SN, RA), 5 = the
+ * 12-warp kernel (SN, RA; the default where its tile rows fit the grid);
+ * SN only: 4 = eagerly evaluated derivatives.  All paths are
  * parity-tested. */
 void fdns_set_kernel_path(int32_t path);
 

@@ -29,8 +29,8 @@ using namespace fdns;
 namespace {
 
 thread_local std::string g_err;
-int g_kernel_path = 0;        // test hook: 0 default, 1 point kernels, 2 8-warp SN,
-                              // 4 eager-local SN, 5 12-warp SN
+int g_kernel_path = 0;        // test hook: 0 default, 1 point kernels, 2 8-warp tiled
+                              // (SN, RA), 4 eager-local SN, 5 12-warp (SN, RA)
 int g_tiled_ctas = 0;         // test hook: force the tiled grid size (0 = one per SM)
 std::atomic<long long> g_launches{0};
 inline void count(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
@@ -913,7 +913,7 @@ struct TileCost {
 #define FDNS_EDGE_SCALE 1.0
 #endif
 inline double edge_scale(int variant) {
-  switch (variant) {
+  switch (variant & 0xff) {   // (launch keys carry the kernel family above bit 8)
     case FDNS_RA: return 0.0;
     case FDNS_SS: return FDNS_EDGE_SCALE / 1.05;
     case FDNS_RS: return FDNS_EDGE_SCALE / 1.1;
@@ -1128,16 +1128,17 @@ int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, 
   return 0;
 }
 
-// SN kernel choice: the 12-warp kernel where its 12-row tiles waste few rows
-// (measured whole RK3 steps: +8% at 256^3, +5.5% at 128^3; at 64^3, where
-// the last tile row holds 4 of 12 rows, -6%, so the 8-warp kernel stays).
+// SN / RA kernel choice: the 12-warp kernel where its 12-row tiles waste few
+// rows (measured whole RK3 steps, SN: +8% at 256^3, +5.5% at 128^3; at 64^3,
+// where the last tile row holds 4 of 12 rows, -6%, so the 8-warp kernel
+// stays; RA: +6.6% at 128^3, +3.9% at 256^3, +6.3% at 512^3).
 inline bool use_t12(const Geom& g) {
   const int rows = (g.n1 + t12::TJ - 1) / t12::TJ * t12::TJ;
   return g.n1 >= 96 && 20 * (rows - g.n1) <= g.n1;
 }
 
-// The 12-warp SN stage kernel (fdns_tiled12.cuh): its own 36 x 16 plane box.
-template <int MODE, int TJ_ = 12>
+// The 12-warp SN / RA stage kernel (fdns_tiled12.cuh): its own 36 x 16 plane box.
+template <int MODE, int TJ_ = 12, int V = FDNS_SN>
 int launch_t12(const double* in, const double* saved, double* out, const Coef& k, const Geom& g,
                double coef, int wrap, int i_lo, int i_hi, cudaStream_t s) {
   using L = t12::Lay<TJ_>;
@@ -1149,19 +1150,19 @@ int launch_t12(const double* in, const double* saved, double* out, const Coef& k
     pf = (g_prefetch_saved && saved != in && saved_map(&ms, saved, g, L::TJ)) ? 1 : 0;
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [] {
-    cudaFuncSetAttribute(t12::k_stage_t12<FDNS_SN, MODE, TJ_>,
+    cudaFuncSetAttribute(t12::k_stage_t12<V, MODE, TJ_>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_BYTES);
     if (L::MINB > 1)
-      cudaFuncSetAttribute(t12::k_stage_t12<FDNS_SN, MODE, TJ_>,
+      cudaFuncSetAttribute(t12::k_stage_t12<V, MODE, TJ_>,
                            cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   });
   const int ntk = (g.n2 + L::TK - 1) / L::TK;
   const int ntj = (g.n1 + L::TJ - 1) / L::TJ;
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
-  const Launch Lc = pick_launch(ntk, ntj, nplanes, wrap, FDNS_SN | 0x100 | (TJ_ << 12), s, true,
+  const Launch Lc = pick_launch(ntk, ntj, nplanes, wrap, V | 0x100 | (TJ_ << 12), s, true,
                                 L::MINB);
-  launch_pdl(t12::k_stage_t12<FDNS_SN, MODE, TJ_>, dim3((unsigned)Lc.ctas), dim3(L::NT),
+  launch_pdl(t12::k_stage_t12<V, MODE, TJ_>, dim3((unsigned)Lc.ctas), dim3(L::NT),
              L::SMEM_BYTES, s, m, ms, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes,
              Lc.aligned, pf, Lc.cuts);
   return 0;
@@ -1176,7 +1177,11 @@ int launch_residual(int variant, const double* in, const double* saved, double* 
   if (variant != FDNS_BL && g_kernel_path != 1 && plane_map(&m, in, g)) {
     int rc = 0;
     switch (variant) {
-      case FDNS_RA: rc = launch_tiled_v<FDNS_RA, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
+      case FDNS_RA:
+        if (g_kernel_path == 5 || (g_kernel_path == 0 && use_t12(g)))
+          rc = launch_t12<MODE, 12, FDNS_RA>(in, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
+        else rc = launch_tiled_v<FDNS_RA, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
+        break;
       case FDNS_RS: rc = launch_tiled_v<FDNS_RS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
       case FDNS_SN:
         if (g_kernel_path == 5 || (g_kernel_path == 0 && use_t12(g)))

@@ -1,4 +1,4 @@
-// fdns_tiled12.cuh -- the 12-warp SN stage kernel.
+// fdns_tiled12.cuh -- the 12-warp SN and RA stage kernel.
 //
 // Same z-marching, TMA-fed scheme as fdns_tiled.cuh (read that first), laid
 // out so that 12 warps fit on an SM instead of 8.  The 8-warp kernel is
@@ -22,6 +22,16 @@
 //
 // 5 x 41.5 KB ring + 2 x 11.9 KB buffers = 231.7 KB of the 227 KB-per-CTA
 // limit (232448 B).
+//
+// RA (round 2) runs on the same layout.  It taps the oldest plane off its
+// own column as well (the mixed terms re-expand D(u0,x0) at in-plane shifts
+// and D(u1,x1), D(u2,x2) on plane i-2), so its buffer set holds, instead of
+// SN's centre-plane derivatives, plane i-2's u0 box, u1 rows and u2 columns,
+// copied before the step barrier (SAccRA12).  167 registers, no spills;
+// whole RK3 steps +6.6% / +3.9% / +6.3% over the 8-warp RA kernel at
+// 128^3 / 256^3 / 512^3.  (A 32 x 10 tile on a 6-slot ring of nine fields,
+// 10 warps, was 7% slower than 8 warps: two of the four schedulers then
+// carry three warps and the step barrier waits for them.)
 #pragma once
 
 #include "fdns_tiled.cuh"
@@ -88,6 +98,37 @@ struct SAcc12 {
   }
 };
 
+// RA accessor: RA also taps the oldest plane off its own column -- the mixed
+// terms DD(u_J, x_O, x_J) with O or J = 0 re-expand D(u0,x0) at in-plane
+// shifts and D(u1,x1), D(u2,x2) on plane i-2 -- so before the step barrier
+// the kernel copies that plane's u0 box, u1 rows and u2 columns into the
+// (double-buffered) buffer set, and the column's own nine values into m2.
+template <class L>
+struct SAccRA12 {
+  static constexpr bool kInternalEnergy = true;
+  static constexpr bool kMaskTaps = true;
+  const double* p[5];   // p[0] unused
+  const double* o0;     // u0 on plane i-2, box pitch PK, at this column
+  const double* o1;     // u1 on plane i-2, pitch TK (box rows x tile columns)
+  const double* o2;     // u2 on plane i-2, pitch PK (tile rows x box columns)
+  double m2[NSF];
+  double gm1;
+  __device__ __forceinline__ double raw(int f, int di, int dj, int dk) const {
+    const int sf = sfield(f);
+    if (di == -2) {
+      if (dj == 0 && dk == 0) return m2[sf];
+      if (f == U0) return o0[dj * L::PK + dk];
+      if (f == U1) return o1[dj * L::TK];
+      return o2[dk];   // U2 (the only other off-column field tapped there)
+    }
+    return p[di + 2][sf * L::PLANE + dj * L::PK + dk];
+  }
+  __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
+    if (f == PF) return gm1 * raw(RHOE_F, di, dj, dk);   // p = gm1 * rho*e
+    return raw(f, di, dj, dk);
+  }
+};
+
 // Accessor over all five window planes in shared memory (the centre-plane
 // buffers, before the step barrier).
 template <class L>
@@ -123,7 +164,7 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
                 const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
                 int64_t total_steps, int wrap_mask, int i_lo, int nplanes, int split,
                 int pf_saved, const int64_t* __restrict__ cuts) {
-  static_assert(V == FDNS_SN, "12-warp kernel: SN");
+  static_assert(V == FDNS_SN || V == FDNS_RA, "12-warp kernel: SN, RA");
   using L = Lay<TJ_>;
   constexpr int TK = L::TK, TJ = L::TJ, NT = L::NT, PK = L::PK, PLANE = L::PLANE;
   constexpr int SLOT = L::SLOT, BU1_N = L::BU1_N, BU2_N = L::BU2_N, BUFSET = L::BUFSET;
@@ -217,6 +258,11 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
           mbar_wait(&bars[slot_of(d)], ((w + d) / NR) & 1);
           stage_arrival<L>(k, sm + slot_of(d) * SLOT, tid);
         }
+        // the oldest plane's rho*e and T, read into m2 below (before the
+        // step barrier), were just converted by other threads: make those
+        // stores visible first (later steps read m2 from a plane converted
+        // four step barriers earlier)
+        __syncthreads();
       } else {
         mbar_wait(&bars[slot_of(4)], ((w + 4) / NR) & 1);
         stage_arrival<L>(k, sm + slot_of(4) * SLOT, tid);
@@ -224,7 +270,20 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
       double* bufs = bufs0 + (w & 1) * BUFSET;
       double* bu1 = bufs + PLANE - 2 * PK;   // row 2 of the box at offset PLANE
       double* bu2 = bufs + PLANE + BU1_N;    // (row, column - 2), pitch TK
-      {
+      if constexpr (V == FDNS_RA) {
+        // plane i-2's u0 box, u1 (box rows x tile columns, pitch TK) and u2
+        // (tile rows x box columns, pitch PK), before its slot is reused
+        const double* old = sm + slot_of(0) * SLOT;
+        double* r1 = bufs + PLANE;             // u1, PJ x TK
+        double* r2 = bufs + PLANE + BU2_N;     // u2, TJ x PK
+        static_assert(BU2_N == L::PJ * TK && BU1_N == TJ * PK, "RA buffer shapes");
+#pragma unroll 1
+        for (int x0 = tid; x0 < PLANE; x0 += NT) bufs[x0] = old[U0 * PLANE + x0];
+#pragma unroll 1
+        for (int y = tid; y < BU2_N; y += NT) r1[y] = old[U1 * PLANE + (y / TK) * PK + 2 + y % TK];
+#pragma unroll 1
+        for (int y = tid; y < BU1_N; y += NT) r2[y] = old[U2 * PLANE + 2 * PK + y];
+      } else {
         const double* base[5];
 #pragma unroll
         for (int d = 0; d < 5; ++d) base[d] = sm + slot_of(d) * SLOT;
@@ -285,7 +344,8 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
       }
       // axis-0 queues of D(u1,x1), D(u2,x2) at this column (before the
       // barrier: at a segment start they read the oldest slot too)
-      if (t == 0) {
+      if constexpr (V != FDNS_SN) {
+      } else if (t == 0) {
 #pragma unroll
         for (int d = 0; d < 5; ++d) {
           SAccW b;
@@ -303,12 +363,18 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
       }
 
       // this column's values on the oldest plane, before its slot is reused
-      SAcc12 a;
+      using Acc = std::conditional_t<V == FDNS_RA, SAccRA12<L>, SAcc12>;
+      Acc a;
       a.gm1 = k.gm1;
       {
         const double* old = sm + slot_of(0) * SLOT + toff;
 #pragma unroll
         for (int f = 0; f < NSF; ++f) a.m2[f] = old[f * PLANE];
+      }
+      if constexpr (V == FDNS_RA) {
+        a.o0 = bufs + toff;
+        a.o1 = bufs + PLANE + (tj + 2) * TK + tk;
+        a.o2 = bufs + PLANE + BU2_N + tj * PK + tk + 2;
       }
       __syncthreads();
       if (w == 0) tiled::trace(2);
@@ -324,7 +390,10 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
 #pragma unroll
       for (int f = 0; f < NFIELDS; ++f) r[f] = a.v(f, 0, 0, 0);   // r[RHOE_F] = rho*e
       double R[5];
-      {
+      if constexpr (V == FDNS_RA) {
+        InlineProvider<Acc> P(k, a);
+        residual_point<true>(k, P, r, R);
+      } else {
         const tiled::TiledLazyProviderT<SAcc12, TK> P{
             k, a, q1, q2, bufs + toff, bu1 + toff, bu2 + (tj + 2) * TK + tk};
         residual_point<true>(k, P, r, R);
