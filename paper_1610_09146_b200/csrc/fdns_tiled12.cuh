@@ -80,6 +80,9 @@ __device__ __forceinline__ constexpr int sfield(int f) { return f == TF ? SF_T :
 // Accessor of the staged window.  Taps at axis-0 offset -2 come from the
 // registers m2 (read before the step barrier: that slot is being refilled by
 // then); the SN provider only taps the oldest plane at its own column.
+#ifndef FDNS_SHFL_X
+#define FDNS_SHFL_X 0
+#endif
 template <class L>
 struct SAcc12 {
   static constexpr bool kInternalEnergy = true;
@@ -90,6 +93,19 @@ struct SAcc12 {
   __device__ __forceinline__ double raw(int f, int di, int dj, int dk) const {
     const int sf = sfield(f);
     if (di == -2) return m2[sf];
+#if FDNS_SHFL_X
+    // A/B of the north star's "warp shuffles for the x-direction taps": a
+    // warp is one 32-point row of the tile (axis 2), so a centre-plane tap
+    // at dk comes from lane + dk's centre value (two 32-bit shuffles), the
+    // edge lanes reading the box halo from shared memory.  Same bits.
+    if (di == 0 && dj == 0 && dk != 0) {
+      const double c = p[2][sf * L::PLANE];
+      const int src = (int)(threadIdx.x & 31) + dk;
+      double s = __shfl_sync(0xffffffffu, c, src & 31);
+      if (src < 0 || src > 31) s = p[2][sf * L::PLANE + dk];
+      return s;
+    }
+#endif
     return p[di + 2][sf * L::PLANE + dj * L::PK + dk];
   }
   __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
