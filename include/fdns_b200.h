@@ -118,8 +118,9 @@ int32_t fdns_stage_planes(int32_t variant, const double* in,
 
 /* Test hook selecting the kernel family: 0 = default (TMA-staged tiled
  * kernels where the row pitch allows), 1 = one-thread-per-point kernels (global-memory
- * taps) for every variant; 2 = the 8-warp tiled kernel (SN, RA), 5 = the
- * 12-warp kernel (SN, RA; the default where its tile rows fit the grid);
+ * taps) for every variant; 2 = the 8-warp tiled kernel (SN, RA, SS, RS),
+ * 5 = the 12-warp kernel (the default for SN and RA where its tile rows fit
+ * the grid, for SS and RS on large planes with the round-robin split);
  * SN only: 4 = eagerly evaluated derivatives.  All paths are
  * parity-tested. */
 void fdns_set_kernel_path(int32_t path);

@@ -838,6 +838,26 @@ bool saved_map(CUtensorMap* m, const double* saved, const Geom& g, int box_j = t
   return r == CUDA_SUCCESS;
 }
 
+// General 4-D box map over `nf` fields of a padded bundle (field stride
+// `fstride` elements), box (bk, bj, 1, bf).
+bool box_map(CUtensorMap* m, const double* base, const Geom& g, int nf, int64_t fstride, int bk,
+             int bj, int bf) {
+  const int64_t P2 = g.n2 + 2 * g.h, P1 = g.n1 + 2 * g.h, P0 = g.n0 + 2 * g.h;
+  if (P2 % 2 != 0 || g.h % 2 != 0) return false;
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0) return false;
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)P2, (cuuint64_t)P1, (cuuint64_t)P0, (cuuint64_t)nf};
+  cuuint64_t strides[3] = {(cuuint64_t)(P2 * 8), (cuuint64_t)(P1 * P2 * 8),
+                           (cuuint64_t)(fstride * 8)};
+  cuuint32_t box[4] = {(cuuint32_t)bk, (cuuint32_t)bj, 1, (cuuint32_t)bf};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Per-device state: a process may drive several GPUs (one per thread or
 // in turn), so every cache below is keyed by the current device.
 constexpr int MAX_DEVICES = 64;
@@ -1137,17 +1157,39 @@ inline bool use_t12(const Geom& g) {
   return g.n1 >= 96 && 20 * (rows - g.n1) <= g.n1;
 }
 
-// The 12-warp SN / RA stage kernel (fdns_tiled12.cuh): its own 36 x 16 plane box.
+// SS / RS on the 12-warp kernel where the round-robin split applies and the
+// planes are large (whole RK3 steps at 512^3: SS +1.8-2.6%, RS +0.2-1.7%;
+// 256^3: SS equal, RS -3%); FDNS_SS_T12=0 keeps the 8-warp kernel (A/B).
+const bool g_ss_t12 = !(std::getenv("FDNS_SS_T12") && std::atoi(std::getenv("FDNS_SS_T12")) == 0);
+inline bool use_t12_ss(int variant, const Geom& g, int nplanes) {
+  return g_ss_t12 && use_t12(g) && (int64_t)g.n1 * g.n2 >= 384 * 384 &&
+         rounds_planes(variant, nplanes) > 0;
+}
+
+// The 12-warp stage kernel (fdns_tiled12.cuh): its own 36 x 16 plane box;
+// SS/RS also the three stored-gradient boxes of the centre plane.
 template <int MODE, int TJ_ = 12, int V = FDNS_SN>
-int launch_t12(const double* in, const double* saved, double* out, const Coef& k, const Geom& g,
-               double coef, int wrap, int i_lo, int i_hi, cudaStream_t s) {
+int launch_t12(const double* in, const double* saved, double* out, const double* work,
+               const Coef& k, const Geom& g, double coef, int wrap, int i_lo, int i_hi,
+               cudaStream_t s) {
   using L = t12::Lay<TJ_>;
+  constexpr bool gb = (V == FDNS_SS || V == FDNS_RS);
   CUtensorMap m, ms;
   if (!plane_map(&m, in, g, L::PJ)) return fail("plane tensor map");
   ms = m;
+  t12::GradMaps gm;
+  for (auto& t : gm.tg) t = m;
+  if constexpr (gb) {
+    if (!box_map(&gm.tg[0], work + 0 * g.fs, g, 1, g.fs, L::PK, L::PJ, 1) ||   // D(u0,x0)
+        !box_map(&gm.tg[1], work + 4 * g.fs, g, 1, g.fs, L::PK, L::TJ, 1) ||   // D(u1,x1)
+        !box_map(&gm.tg[2], work + 8 * g.fs, g, 1, g.fs, L::TK, L::PJ, 1) ||   // D(u2,x2)
+        !box_map(&gm.tg[3], work, g, 9, g.fs, L::TK, L::TJ, 9))
+      return fail("gradient tensor map");
+  }
   int pf = 0;
   if constexpr (MODE == 1)
-    pf = (g_prefetch_saved && saved != in && saved_map(&ms, saved, g, L::TJ)) ? 1 : 0;
+    pf = (g_prefetch_saved && saved != in && saved_map(&ms, saved, g, L::TJ)) ? tiled::PF_SAVED : 0;
+  if constexpr (gb) pf |= g_prefetch_grad ? tiled::PF_GRAD : 0;
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [] {
     cudaFuncSetAttribute(t12::k_stage_t12<V, MODE, TJ_>,
@@ -1160,11 +1202,25 @@ int launch_t12(const double* in, const double* saved, double* out, const Coef& k
   const int ntj = (g.n1 + L::TJ - 1) / L::TJ;
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
+  if constexpr (gb) {
+    if (const int c = rounds_planes(V, nplanes)) {   // round-robin units (SS/RS)
+      static std::atomic<uint64_t> attr_rr{0};
+      once_per_device(attr_rr, [] {
+        cudaFuncSetAttribute(t12::k_stage_t12<V, MODE, TJ_, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_BYTES);
+      });
+      launch_pdl(t12::k_stage_t12<V, MODE, TJ_, true>,
+                 dim3((unsigned)std::min<int64_t>(num_sms(), total / c)), dim3(L::NT),
+                 L::SMEM_BYTES, s, m, ms, gm, work, saved, out, k, g, coef, ntk, total, wrap,
+                 i_lo, c, (int)tiled::SPLIT_ROUNDS, pf, (const int64_t*)nullptr);
+      return 0;
+    }
+  }
   const Launch Lc = pick_launch(ntk, ntj, nplanes, wrap, V | 0x100 | (TJ_ << 12), s, true,
                                 L::MINB);
   launch_pdl(t12::k_stage_t12<V, MODE, TJ_>, dim3((unsigned)Lc.ctas), dim3(L::NT),
-             L::SMEM_BYTES, s, m, ms, saved, out, k, g, coef, ntk, total, wrap, i_lo, nplanes,
-             Lc.aligned, pf, Lc.cuts);
+             L::SMEM_BYTES, s, m, ms, gm, work, saved, out, k, g, coef, ntk, total, wrap, i_lo,
+             nplanes, Lc.aligned, pf, Lc.cuts);
   return 0;
 }
 
@@ -1179,18 +1235,26 @@ int launch_residual(int variant, const double* in, const double* saved, double* 
     switch (variant) {
       case FDNS_RA:
         if (g_kernel_path == 5 || (g_kernel_path == 0 && use_t12(g)))
-          rc = launch_t12<MODE, 12, FDNS_RA>(in, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
+          rc = launch_t12<MODE, 12, FDNS_RA>(in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
         else rc = launch_tiled_v<FDNS_RA, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
         break;
-      case FDNS_RS: rc = launch_tiled_v<FDNS_RS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
+      case FDNS_RS:
+        if (g_kernel_path == 5 || (g_kernel_path == 0 && use_t12_ss(FDNS_RS, g, i_hi - i_lo)))
+          rc = launch_t12<MODE, 12, FDNS_RS>(in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
+        else rc = launch_tiled_v<FDNS_RS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
+        break;
       case FDNS_SN:
         if (g_kernel_path == 5 || (g_kernel_path == 0 && use_t12(g)))
-          rc = launch_t12<MODE>(in, saved, out, k, g, coef, wrap, i_lo, i_hi, s);
+          rc = launch_t12<MODE>(in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
         else if (g_kernel_path == 4)
           rc = launch_tiled_v<FDNS_SN, MODE, false>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
         else rc = launch_tiled_v<FDNS_SN, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
         break;
-      case FDNS_SS: rc = launch_tiled_v<FDNS_SS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s); break;
+      case FDNS_SS:
+        if (g_kernel_path == 5 || (g_kernel_path == 0 && use_t12_ss(FDNS_SS, g, i_hi - i_lo)))
+          rc = launch_t12<MODE, 12, FDNS_SS>(in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
+        else rc = launch_tiled_v<FDNS_SS, MODE>(m, in, saved, out, work, k, g, coef, wrap, i_lo, i_hi, s);
+        break;
       default: return fail("unknown variant");
     }
     if (rc) return rc;   // e.g. a tensor map that could not be encoded

@@ -343,15 +343,15 @@ using TiledLazyProvider = TiledLazyProviderT<SAcc, PK>;
 // gradients at the point are loaded at step start.  Every value is read from
 // the work arrays (FETCH, plan.py:176-179); mixed terms apply the outer
 // stencil to the stored inner values exactly as codegen.py:111-113 does.
-template <bool INLINE_REST>
-struct TiledSSProvider {
+template <bool INLINE_REST, class A, int B2P>
+struct TiledSSProviderT {
   const Coef& k;
-  const SAcc& a;
+  const A& a;
   const double* q1;   // stored D(u1,x1) at this column, planes i-2..i+2
   const double* q2;   // stored D(u2,x2)
   const double* gb0;  // stored D(u0,x0), centre of the box (pitch PK)
   const double* gb1;  // stored D(u1,x1)
-  const double* gb2;  // stored D(u2,x2)
+  const double* gb2;  // stored D(u2,x2) (row pitch B2P)
   const double* gv;   // off-diagonal D(u_q,x_a) at the point, [q*3+a]
   template <int A_, int L, int OCC = 0>
   __device__ __forceinline__ double g() const {
@@ -374,12 +374,14 @@ struct TiledSSProvider {
       constexpr int s = O == 1 ? PK : 1;
       return k.w1[O] * (gb0[s] - gb0[-s]) + k.w2[O] * (gb0[2 * s] - gb0[-2 * s]);
     } else if constexpr (J == 2) {
-      return k.w1[1] * (gb2[PK] - gb2[-PK]) + k.w2[1] * (gb2[2 * PK] - gb2[-2 * PK]);
+      return k.w1[1] * (gb2[B2P] - gb2[-B2P]) + k.w2[1] * (gb2[2 * B2P] - gb2[-2 * B2P]);
     } else {
       return k.w1[2] * (gb1[1] - gb1[-1]) + k.w2[2] * (gb1[2] - gb1[-2]);
     }
   }
 };
+template <bool INLINE_REST>
+using TiledSSProvider = TiledSSProviderT<INLINE_REST, SAcc, PK>;
 
 // Static, balanced work split of one stage: the (tile, plane) steps in
 // tile-major order are cut into gridDim.x equal ranges; a CTA walks its

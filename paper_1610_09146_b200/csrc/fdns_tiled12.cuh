@@ -1,4 +1,4 @@
-// fdns_tiled12.cuh -- the 12-warp SN and RA stage kernel.
+// fdns_tiled12.cuh -- the 12-warp stage kernel (SN, RA; SS/RS on large planes).
 //
 // Same z-marching, TMA-fed scheme as fdns_tiled.cuh (read that first), laid
 // out so that 12 warps fit on an SM instead of 8.  The 8-warp kernel is
@@ -22,6 +22,16 @@
 //
 // 5 x 41.5 KB ring + 2 x 11.9 KB buffers = 231.7 KB of the 227 KB-per-CTA
 // limit (232448 B).
+//
+// SS / RS (round 2) run on it from 384^2-point planes, where the round-robin
+// split applies (see fdns_b200.cu:use_t12_ss): their buffer set is the three
+// TMA boxes of the centre plane's stored diagonal gradients; the axis-0
+// queues and the six off-diagonal gradients are per-thread loads, as in the
+// 8-warp kernel.  Whole RK3 steps at 512^3: SS +1.8-2.6%, RS +0.2-1.7%; at
+// 256^3 SS equal, RS -3%; without the round-robin split 6-11% slower (more
+// DRAM traffic; profiles/r02_ss_t12_ab.txt).  There is no shared memory left
+// to stage the off-diagonal gradients, so its load/store unit is busier
+// than SN's (mio + lg throttle stalls ~0.8 vs ~0.4 cycles per instruction).
 //
 // RA (round 2) runs on the same layout.  It taps the oldest plane off its
 // own column as well (the mixed terms re-expand D(u0,x0) at in-plane shifts
@@ -174,13 +184,25 @@ __device__ __forceinline__ void stage_arrival(const Coef& k, double* slot, int t
   }
 }
 
-template <int V, int MODE, int TJ_ = 12>
+// SS / RS: the three TMA boxes of the centre plane's stored diagonal
+// gradients, laid out like SN's buffer set: D(u0,x0) over the whole box,
+// D(u1,x1) over the tile rows (pitch PK), D(u2,x2) over the tile columns
+// (pitch TK).  tg[0..2] are their tensor maps, tg[3] the L2-prefetch box of
+// all nine stored gradients of a plane's tile columns.
+struct GradMaps {
+  CUtensorMap tg[4];
+};
+
+template <int V, int MODE, int TJ_ = 12, bool RR = false>
 __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
     k_stage_t12(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tsv,
+                const __grid_constant__ GradMaps gm, const double* __restrict__ work,
                 const double* saved, double* out, Coef k, Geom g, double coef, int ntk,
                 int64_t total_steps, int wrap_mask, int i_lo, int nplanes, int split,
                 int pf_saved, const int64_t* __restrict__ cuts) {
-  static_assert(V == FDNS_SN || V == FDNS_RA, "12-warp kernel: SN, RA");
+  static_assert(V == FDNS_SN || V == FDNS_RA || V == FDNS_SS || V == FDNS_RS,
+                "12-warp kernel variant");
+  constexpr bool kGB = (V == FDNS_SS || V == FDNS_RS);
   using L = Lay<TJ_>;
   constexpr int TK = L::TK, TJ = L::TJ, NT = L::NT, PK = L::PK, PLANE = L::PLANE;
   constexpr int SLOT = L::SLOT, BU1_N = L::BU1_N, BU2_N = L::BU2_N, BUFSET = L::BUFSET;
@@ -190,15 +212,31 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
   extern __shared__ __align__(128) double sm[];
   double* bufs0 = sm + NR * SLOT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NR * SLOT + 2 * BUFSET);
+  uint64_t* gbars = bars + NR;   // SS/RS: the gradient boxes of the two buffer sets
   const int tid = threadIdx.x;
   const int tk = tid % TK, tj = tid / TK;
   Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes, split, cuts);
+  if constexpr (RR) S.tiles = (int64_t)ntk * ((g.n1 + TJ - 1) / TJ);
+  // segment walk: contiguous tile-major ranges, or (RR) round-robin units
+  auto seg_next = [&](int64_t x) -> int64_t {
+    if constexpr (RR) return S.next(x);
+    else return S.seg_end(x);
+  };
+  auto tile_at = [&](int64_t x) -> int64_t {
+    if constexpr (RR) return S.tile_of(x);
+    else return x / nplanes;
+  };
+  auto plane_at = [&](int64_t x) -> int {
+    if constexpr (RR) return S.plane_of(x);
+    else return (int)(x % nplanes);
+  };
   if (S.beg >= S.end) return;
   tiled::trace(0);
 
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < NR; ++s) mbar_init(&bars[s], 1);
+    if constexpr (kGB) { mbar_init(&gbars[0], 1); mbar_init(&gbars[1], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -206,33 +244,53 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   tiled::trace(1);
 
+  // SS/RS: the stored-gradient boxes of the centre plane of step gs
+  auto issue_gb_tile = [&](int gs_, int k0, int j0, int plane) {
+    double* dst = bufs0 + (gs_ & 1) * BUFSET;
+    uint64_t* bar = &gbars[gs_ & 1];
+    mbar_expect_tx(bar, BUFSET * 8);
+    tma_load_plane(dst, &gm.tg[0], bar, k0 + g.h - 2, j0 + g.h - 2, plane + g.h);
+    tma_load_plane(dst + PLANE, &gm.tg[1], bar, k0 + g.h - 2, j0 + g.h, plane + g.h);
+    tma_load_plane(dst + PLANE + BU1_N, &gm.tg[2], bar, k0 + g.h, j0 + g.h - 2, plane + g.h);
+  };
+  auto issue_gb = [&](int gs_, int64_t x) {
+    const int64_t tile = tile_at(x);
+    issue_gb_tile(gs_, (int)(tile % ntk) * TK, (int)(tile / ntk) * TJ, i_lo + plane_at(x));
+  };
+  if constexpr (kGB)
+    if (tid == 0) issue_gb(0, S.beg);
+  int gs = 0;   // steps of this CTA: buffer-set parity
+
   // producer cursor (thread 0), as in k_stage_tiled
   int64_t p_seg = S.beg;
   int p_r = 0, issued = 0;
   int p_len = 0, p_c0 = 0, p_c1 = 0, p_plane = 0, p_slot = 0;
   auto enter_segment = [&]() {
-    const int64_t tile = p_seg / nplanes;
+    const int64_t tile = tile_at(p_seg);
     p_len = (int)(S.seg_end(p_seg) - p_seg) + 4;
     p_c0 = (int)(tile % ntk) * TK + g.h - 2;
     p_c1 = (int)(tile / ntk) * TJ + g.h - 2;
-    p_plane = i_lo + (int)(p_seg % nplanes) - 2 + g.h;
+    p_plane = i_lo + plane_at(p_seg) - 2 + g.h;
   };
   if (tid == 0) enter_segment();
   auto issue_next = [&]() {
     mbar_expect_tx(&bars[p_slot], LOAD_BYTES);
     tma_load_plane(sm + p_slot * SLOT, &tin, &bars[p_slot], p_c0, p_c1, p_plane + p_r);
-    if (MODE == 1 && pf_saved && p_r >= 2 && p_r < p_len - 2)
+    if (MODE == 1 && (pf_saved & tiled::PF_SAVED) && p_r >= 2 && p_r < p_len - 2)
       tma_prefetch_l2(&tsv, p_c0 + 2, p_c1 + 2, p_plane + p_r);
+    // SS/RS: the nine stored gradients of this plane's tile columns into L2
+    if constexpr (kGB)
+      if (pf_saved & tiled::PF_GRAD) tma_prefetch_l2(&gm.tg[3], p_c0 + 2, p_c1 + 2, p_plane + p_r);
     ++issued;
     p_slot = p_slot + 1 == NR ? 0 : p_slot + 1;
     if (++p_r == p_len) {
       p_r = 0;
-      p_seg = S.seg_end(p_seg);
+      p_seg = seg_next(p_seg);
       if (p_seg < S.end) enter_segment();
     }
   };
   int total_pos = 0;
-  for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) total_pos += (int)(S.seg_end(x) - x) + 4;
+  for (int64_t x = S.beg; x < S.end; x = seg_next(x)) total_pos += (int)(S.seg_end(x) - x) + 4;
   if (tid == 0)
     while (issued < total_pos && issued < NR) issue_next();
 
@@ -241,17 +299,17 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
     const int x = wsl + d;
     return x >= NR ? x - NR : x;
   };
-  for (int64_t x = S.beg; x < S.end; x = S.seg_end(x)) {
+  for (int64_t x = S.beg; x < S.end; x = seg_next(x)) {
     const int64_t se = S.seg_end(x);
-    const int64_t tile = x / nplanes;
+    const int64_t tile = tile_at(x);
     const int k0 = (int)(tile % ntk) * TK, j0 = (int)(tile / ntk) * TJ;
     const int jj = j0 + tj, kk = k0 + tk;
     const bool active = jj < g.n1 && kk < g.n2;
     const int toff = (tj + 2) * PK + (tk + 2);
     const int nsteps = (int)(se - x);
-    const int i_seg = i_lo + (int)(x % nplanes);
+    const int i_seg = i_lo + plane_at(x);
     double q1[5], q2[5];
-    for (int t = 0; t < nsteps; ++t, ++w, wsl = (wsl + 1 == NR ? 0 : wsl + 1)) {
+    for (int t = 0; t < nsteps; ++t, ++w, ++gs, wsl = (wsl + 1 == NR ? 0 : wsl + 1)) {
       if (t == 0 && w > 0) {
         // segment change: the new window's five planes; the ring slots of
         // the previous segment are free once every thread is past it
@@ -269,6 +327,35 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
 #pragma unroll
         for (int f = 0; f < 5; ++f) sv[f] = saved[f * g.fs + cl];
       }
+      // SS/RS: the stored gradients this point FETCHes (plan.py:176-179):
+      // the axis-0 queues of D(u1,x1), D(u2,x2) at this column and the six
+      // off-diagonal D(u_q,x_a) at the point, issued early so their latency
+      // runs under the arrival conversion and the barrier
+      double gv[9];
+      if constexpr (kGB) {
+        const double* w11 = work + 4 * g.fs + cl;
+        const double* w22 = work + 8 * g.fs + cl;
+        if (t == 0) {
+#pragma unroll
+          for (int d = 0; d < 5; ++d) {
+            q1[d] = __ldg(w11 + (d - 2) * g.s0);
+            q2[d] = __ldg(w22 + (d - 2) * g.s0);
+          }
+        } else {
+#pragma unroll
+          for (int d = 0; d < 4; ++d) { q1[d] = q1[d + 1]; q2[d] = q2[d + 1]; }
+          q1[4] = __ldg(w11 + 2 * g.s0);
+          q2[4] = __ldg(w22 + 2 * g.s0);
+        }
+      }
+      if constexpr (kGB) {
+        gv[0 * 3 + 1] = __ldg(work + 1 * g.fs + cl);
+        gv[0 * 3 + 2] = __ldg(work + 2 * g.fs + cl);
+        gv[1 * 3 + 0] = __ldg(work + 3 * g.fs + cl);
+        gv[1 * 3 + 2] = __ldg(work + 5 * g.fs + cl);
+        gv[2 * 3 + 0] = __ldg(work + 6 * g.fs + cl);
+        gv[2 * 3 + 1] = __ldg(work + 7 * g.fs + cl);
+      }
       if (t == 0) {
         for (int d = 0; d < 5; ++d) {
           mbar_wait(&bars[slot_of(d)], ((w + d) / NR) & 1);
@@ -283,7 +370,7 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
         mbar_wait(&bars[slot_of(4)], ((w + 4) / NR) & 1);
         stage_arrival<L>(k, sm + slot_of(4) * SLOT, tid);
       }
-      double* bufs = bufs0 + (w & 1) * BUFSET;
+      double* bufs = bufs0 + (gs & 1) * BUFSET;
       double* bu1 = bufs + PLANE - 2 * PK;   // row 2 of the box at offset PLANE
       double* bu2 = bufs + PLANE + BU1_N;    // (row, column - 2), pitch TK
       if constexpr (V == FDNS_RA) {
@@ -299,6 +386,8 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
         for (int y = tid; y < BU2_N; y += NT) r1[y] = old[U1 * PLANE + (y / TK) * PK + 2 + y % TK];
 #pragma unroll 1
         for (int y = tid; y < BU1_N; y += NT) r2[y] = old[U2 * PLANE + 2 * PK + y];
+      } else if constexpr (kGB) {
+        // stored gradient boxes: TMA (issue_gb_tile)
       } else {
         const double* base[5];
 #pragma unroll
@@ -394,9 +483,15 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
       }
       __syncthreads();
       if (w == 0) tiled::trace(2);
-      if (tid == 0 && issued < total_pos && issued < w + NR + 1) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_next();   // the next plane, into the oldest slot
+      if (tid == 0) {
+        if (issued < total_pos && issued < w + NR + 1) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue_next();   // the next plane, into the oldest slot
+        }
+        if constexpr (kGB) {   // the next step's gradient boxes, other buffer set
+          if (t + 1 < nsteps) issue_gb_tile(gs + 1, k0, j0, i + 1);
+          else if (seg_next(x) < S.end) issue_gb(gs + 1, seg_next(x));
+        }
       }
 #pragma unroll
       for (int d = 0; d < 5; ++d) a.p[d] = sm + slot_of(d) * SLOT + toff;
@@ -408,6 +503,11 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
       double R[5];
       if constexpr (V == FDNS_RA) {
         InlineProvider<Acc> P(k, a);
+        residual_point<true>(k, P, r, R);
+      } else if constexpr (kGB) {
+        mbar_wait(&gbars[gs & 1], (gs >> 1) & 1);
+        const tiled::TiledSSProviderT<V == FDNS_RS, Acc, TK> P{
+            k, a, q1, q2, bufs + toff, bu1 + toff, bu2 + (tj + 2) * TK + tk, gv};
         residual_point<true>(k, P, r, R);
       } else {
         const tiled::TiledLazyProviderT<SAcc12, TK> P{

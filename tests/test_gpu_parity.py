@@ -458,12 +458,13 @@ def kernel_path():
     lib.fdns_set_tiled_grid(0)
 
 
-@pytest.mark.parametrize("variant,path", [(v, 0) for v in VARIANTS] + [("SN", 5), ("RA", 5)])
+@pytest.mark.parametrize("variant,path", [(v, 0) for v in VARIANTS] + [("SN", 5), ("RA", 5),
+                                                                        ("SS", 5), ("RS", 5)])
 @pytest.mark.parametrize("ctas", [3, 7, 13])
 def test_tiled_segment_transitions(kernel_path, variant, ctas, path):
     """Force the persistent tiled kernel onto few CTAs so each walks several
     (tile, plane-range) segments; results stay bitwise equal to the
-    one-thread-per-point path.  Path 5 runs SN and RA on the 12-warp kernel (at
+    one-thread-per-point path.  Path 5 runs SN, RA, SS and RS on the 12-warp kernel (at
     this size the default picks the 8-warp one)."""
     npts = (21, 20, 34)
     F = npo.state_from_primitives(npts, CO, np.ones(npts) + 0.01 * np.arange(
@@ -506,7 +507,8 @@ def test_sn_kernel_families_agree(kernel_path, ctas):
 
 # ------------------------------------------------ decomposition invariance
 @pytest.mark.parametrize("variant,path", [("SN", 0), ("SS", 0), ("BL", 0), ("RA", 0),
-                                          ("SN", 5), ("RA", 5)])
+                                          ("SN", 5), ("RA", 5), ("SS", 5),
+                                          ("RS", 5)])
 @pytest.mark.parametrize("nranks", [2, 3])
 @pytest.mark.parametrize("split", [False, True])
 def test_slab_decomposition_bitwise_invariant(kernel_path, variant, nranks, split, path):
@@ -516,7 +518,7 @@ def test_slab_decomposition_bitwise_invariant(kernel_path, variant, nranks, spli
     after every stage, as Slab.exchange does over NCCL.  The ranks' kernels
     never wait on each other (the host sequences stage -> exchange), so this
     is a faithful single-GPU emulation.  Fields must equal the one-GPU run
-    bitwise.  Path 5 runs SN and RA on the 12-warp kernel (plane-range launches of
+    bitwise.  Path 5 runs SN, RA, SS and RS on the 12-warp kernel (plane-range launches of
     the boundary/interior split included)."""
     n0, n1, n2, h = 24, 16, 20, 2
     npts = (n0, n1, n2)
