@@ -141,10 +141,9 @@ void fdns_set_pdl(int32_t enabled);
  * stored gradients.  A kill switch and an A/B hook. */
 void fdns_set_prefetch(int32_t mask);
 
-/* Test hook: unit size (planes) of the round-robin split of SS/RS and of
- * SN on the 12-warp kernel (-1 = defaults: SS/RS 64-plane units from 256
- * planes, SN 128-plane units from 512 planes; 0 = off; c > 0 = c-plane
- * units wherever the plane count is a multiple of c and at least 4c). */
+/* Test hook: unit size (planes) of the SS/RS round-robin split (-1 =
+ * default: 64-plane units from 256 planes; 0 = off; c > 0 = c-plane units
+ * wherever the plane count is a multiple of c and at least 4c). */
 void fdns_set_rounds(int32_t planes);
 
 /* Debug timeline of the tiled stage kernels: enable (1) / disable (0) the

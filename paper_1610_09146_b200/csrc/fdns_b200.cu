@@ -1028,18 +1028,15 @@ struct Launch { int64_t ctas; int aligned; const int64_t* cuts; };
 // -1.7%), and SN/RA (FP64-bound, far from the HBM roof) lose 5-9% at every
 // size, so only SS/RS from 256 planes use it.  FDNS_ROUNDS=C overrides the
 // unit (0 disables).
-// Round 2, 12-warp kernel: SN with 128-plane units from 512 planes (DRAM
-// reads 31.4 -> ~25 GB per stage at 512^3, whole steps +3.0%; 64-plane units
-// +2.2% at 512^3 but -6% at 256^3); RA gains nothing (-0.4%), so it keeps
-// the contiguous split.  FDNS_ROUNDS_SN=C overrides the SN unit.
-constexpr int ROUND_PLANES = 64, ROUND_PLANES_SN = 128;
+// Round 2, 12-warp kernel: SN with 64/128-plane units cut its DRAM reads
+// (31.4 -> ~25 GB per stage at 512^3) but its step time moved by -0.1% to
+// +3% depending on the box (profiles/r02_rr_sn_ra_ab.txt), RA by -0.4%:
+// both keep the contiguous split.
+constexpr int ROUND_PLANES = 64;
 int g_rounds_env = std::getenv("FDNS_ROUNDS") ? std::atoi(std::getenv("FDNS_ROUNDS")) : -1;
-int g_rounds_sn = std::getenv("FDNS_ROUNDS_SN") ? std::atoi(std::getenv("FDNS_ROUNDS_SN")) : -1;
 inline int rounds_planes(int variant, int nplanes) {
-  int c;
-  if (variant == FDNS_SS || variant == FDNS_RS) c = g_rounds_env >= 0 ? g_rounds_env : ROUND_PLANES;
-  else if (variant == FDNS_SN) c = g_rounds_sn >= 0 ? g_rounds_sn : ROUND_PLANES_SN;   // 12-warp kernel
-  else return 0;
+  if (variant != FDNS_SS && variant != FDNS_RS) return 0;
+  const int c = g_rounds_env >= 0 ? g_rounds_env : ROUND_PLANES;
   if (c <= 0 || nplanes % c != 0 || nplanes < 4 * c || g_tiled_ctas > 0) return 0;
   return c;
 }
@@ -1209,8 +1206,8 @@ int launch_t12(const double* in, const double* saved, double* out, const double*
   const int ntj = (g.n1 + L::TJ - 1) / L::TJ;
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
-  if constexpr (V != FDNS_RA) {
-    if (const int c = rounds_planes(V, nplanes)) {   // round-robin units (SN, SS, RS)
+  if constexpr (gb) {
+    if (const int c = rounds_planes(V, nplanes)) {   // round-robin units (SS/RS)
       static std::atomic<uint64_t> attr_rr{0};
       once_per_device(attr_rr, [] {
         cudaFuncSetAttribute(t12::k_stage_t12<V, MODE, TJ_, true>,
@@ -1403,7 +1400,7 @@ void fdns_set_tiled_grid(int32_t ctas) { g_tiled_ctas = ctas; }
 
 void fdns_set_pdl(int32_t enabled) { g_pdl = enabled != 0; }
 
-void fdns_set_rounds(int32_t planes) { g_rounds_env = planes; g_rounds_sn = planes; }
+void fdns_set_rounds(int32_t planes) { g_rounds_env = planes; }
 
 void fdns_set_prefetch(int32_t mask) {
   g_prefetch_saved = (mask & 1) != 0;
