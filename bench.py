@@ -185,26 +185,51 @@ def cpu_cores() -> int:
     return len(os.sched_getaffinity(0))
 
 
+def weak_factors(world: int) -> tuple:
+    """Grid scale factors of a weak-scaling run on `world` GPUs: the
+    reference's decompose_workers (pkg/src/fdns/bench.py:160-173; the same
+    rule as benchtables.decompose_workers, kept here so the reference arm
+    needs no package import): 8 GPUs scale n^3 to (2n)^3, so C5's 512^3 on
+    one GPU meets its 1024^3 8-GPU counterpart (BASELINE.json configs[4])."""
+    factors, w, d, primes = [1, 1, 1], world, 2, []
+    while w > 1:
+        while w % d == 0:
+            primes.append(d)
+            w //= d
+        d += 1
+    for p in sorted(primes, reverse=True):
+        factors[factors.index(min(factors))] *= p
+    return tuple(sorted(factors, reverse=True))
+
+
 def global_grid(args, world: int) -> tuple:
-    """Global grid points: n^3, or (n*world, n, n) for weak scaling."""
+    """Global grid points: n^3, or n x weak_factors(world) for weak scaling
+    (slabs are still cut along axis 0)."""
     n = args.n
     if world > 1 and args.scaling == "weak":
-        return (n * world, n, n)
+        return tuple(n * f for f in weak_factors(world))
     return (n, n, n)
+
+
+def dt_of(npts) -> float:
+    """RK3 step of a grid: the configs' dt of its finest axis."""
+    return DT.get(max(npts), 3.385e-3)
 
 
 def config_dict(args, world: int) -> dict:
     """The workload description both arms print (identical by construction)."""
     npts = global_grid(args, world)
     n = args.n
-    name = CONFIG_NAMES.get(n, "custom")
-    weak = npts[0] != n
+    weak = tuple(npts) != (n, n, n)
+    name = CONFIG_NAMES.get(max(npts) if weak and len(set(npts)) == 1 else n, "custom")
+    if weak and len(set(npts)) != 1:
+        name += f" weak x{world}"
     return {"workload": f"{name}: TGV {'x'.join(map(str, npts))} fp64, "
-                        f"dt={DT.get(n)}, RK3 steps, variants "
+                        f"dt={dt_of(npts)}, RK3 steps, variants "
                         + "/".join(args.variants)
                         + (f", z-slab over {world} GPUs ({args.scaling} "
                            "scaling)" if world > 1 else ""),
-            "grid": list(npts), "dt": DT.get(n),
+            "grid": list(npts), "dt": dt_of(npts),
             "variants": list(args.variants),
             "parallelism": f"z-slab x{world}" + (" (weak)" if weak else ""),
             "l2": "inputs larger than L2 (1.1 GB per 512^3 field); L2 also "
@@ -251,7 +276,7 @@ def bench_variant(fd, variant, grid, cons_host, steps, warmup, flush_buf, lib,
     c = fd.PhysicalConstants()
     state = fresh_state(fd, grid, cons_host)
     ev = fd.ResidualEvaluator(grid, c, variant)
-    scheme = fd.RKScheme(dt=DT.get(grid.npoints[1], 3.385e-3))
+    scheme = fd.RKScheme(dt=dt_of(grid.npoints))
     it = IterationState(state, saved=False)
     multi = grid.slab is not None and grid.slab.nranks > 1
     for _ in range(warmup):
@@ -484,7 +509,7 @@ def bench_e2e(fd, variant, grid, cons_host, steps):
     c = fd.PhysicalConstants()
     state = fresh_state(fd, grid, cons_host)
     ev = fd.ResidualEvaluator(grid, c, variant)
-    scheme = fd.RKScheme(dt=DT.get(grid.npoints[1], 3.385e-3))
+    scheme = fd.RKScheme(dt=dt_of(grid.npoints))
     host = HostStepper.pinned_buffers(grid)
     host.copy_(state.bundle[:5].cpu())
     stepper = HostStepper(state, ev, scheme, host, chunks=E2E_CHUNKS)
@@ -728,8 +753,14 @@ def main_reference(args):
     npts = global_grid(args, world)
     # each "step" is one RK3 iteration of the configured grid; the timed
     # sample is at least --cpu-seconds of them (a 512^3 iteration is
-    # ~8-10 s on 16 cores, so the sample is a bounded number of iterations)
-    val, sec, iters = run_cpu_oracle(npts, 1, warmup=args.cpu_warmup,
+    # ~8-10 s on 16 cores, so the sample is a bounded number of iterations).
+    # A weak-scaled grid beyond 512^3 points (1024^3 on 8 GPUs: 86 GB of
+    # host fields) is sampled on one rank's slab of it (the CPU rate per
+    # point does not depend on the grid at these sizes).
+    sample = npts
+    if float(np.prod(npts)) > 512.0 ** 3:
+        sample = (max(4, npts[0] // world), npts[1], npts[2])
+    val, sec, iters = run_cpu_oracle(sample, 1, warmup=args.cpu_warmup,
                                      min_seconds=args.cpu_seconds)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
@@ -739,13 +770,13 @@ def main_reference(args):
         "scaling": args.scaling if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: analytic Taylor-Green vortex initial state"
-                if len(set(npts)) == 1 else
+                if len(set(sample)) == 1 else
                 "synthetic: smooth manufactured state of the slab grid's shape",
         "config": config_dict(args, world),
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cpu_cores(),
                          "kind": "port",
                          "sample": f"C+OpenMP restatement of the reference "
-                                   f"(SN route), grid {list(npts)}, {iters} "
+                                   f"(SN route), grid {list(sample)}, {iters} "
                                    f"RK3 iterations after {args.cpu_warmup} "
                                    f"warm-up, {sec:.1f} s, rank 0 only"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,

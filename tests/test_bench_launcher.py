@@ -47,7 +47,17 @@ def test_config_identical_between_arms():
     assert s["grid"] == [512, 512, 512]                           # strong
     w = bench.config_dict(bench.parse_args(["--gpus", "8", "--scaling",
                                             "weak"]), 8)
-    assert w["grid"] == [4096, 512, 512]
+    assert w["grid"] == [1024, 1024, 1024] and w["dt"] == 2.1e-4    # C5 weak
+    assert w["workload"].startswith("C5 (weak counterpart)")
+    w2 = bench.config_dict(bench.parse_args(["--gpus", "2", "--scaling",
+                                             "weak"]), 2)
+    assert w2["grid"] == [1024, 512, 512] and w2["dt"] == 2.1e-4
+
+
+def test_weak_factors_match_decompose_workers():
+    from paper_1610_09146_b200.benchtables import decompose_workers
+    for n in range(1, 13):
+        assert bench.weak_factors(n) == decompose_workers(n)
 
 
 @pytest.mark.parametrize("gpus", [2, 3])
