@@ -138,9 +138,12 @@ class ClockSampler:
                  "sw_power_cap"]
         reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:6])
                           if v.lower() == "active"})
+        pw = [float(r[6]) for r in self.rows
+              if len(r) > 6 and r[6].replace(".", "").isdigit()]
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows),
+                "power_w": float(np.median(pw)) if pw else None}
 
 
 # ------------------------------------------------------------------ setup
@@ -489,6 +492,11 @@ def median_mhz(rows):
     return float(np.median(sm)) if sm else None
 
 
+def median_watts(rows):
+    pw = [float(r[6]) for r in rows if len(r) > 6 and r[6].replace(".", "").isdigit()]
+    return float(np.median(pw)) if pw else None
+
+
 # FP64 lanes per SM per clock: the burst probe's 18.5 T instr/s at 1965 MHz
 # over 148 SMs is 63.7
 FP64_PER_SM_CLK = 64
@@ -658,6 +666,7 @@ def main_ours(args):
             fd, v, grid, cons_host, args.steps, args.warmup, flush, lib,
             clocks, args.clock_window)
         v_mhz = median_mhz(clocks.rows[n_rows:])
+        v_watts = median_watts(clocks.rows[n_rows:])
         if world > 1:
             import torch.distributed as dist
             t = torch.tensor([total_ms, cold_ms], device="cuda")
@@ -683,7 +692,7 @@ def main_ours(args):
             "achieved_tflops": flops, "achieved_gbs": gbs,
             "bound": bound, "local_pts": local_pts,
             "roofline_pt_stage_per_s": 1.0 / max(t_fp64, t_hbm),
-            "sm_mhz": v_mhz,
+            "sm_mhz": v_mhz, "power_w": v_watts,
         }
         rec["roofline"] = variant_roofline(v, rec, fp64_tf, hbm_peak,
                                            hbm_src, n, fp64_sus, sms)

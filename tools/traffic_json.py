@@ -14,7 +14,8 @@ import os
 import subprocess
 import sys
 
-VARIANT_OF = [("k_stage_t12<3", "SN"), ("k_stage_t12<1", "RA"), ("k_stage_tiled<1,", "RA"), ("k_stage_tiled<3,", "SN"),
+VARIANT_OF = [("k_stage_t12<3", "SN"), ("k_stage_t12<1", "RA"), ("k_stage_t12<4", "SS"),
+              ("k_stage_t12<2", "RS"), ("k_stage_tiled<1,", "RA"), ("k_stage_tiled<3,", "SN"),
               ("k_stage_tiled<4,", "SS"), ("k_stage_tiled<2,", "RS"), ("k_residual<0,", "BL")]
 
 
