@@ -20,6 +20,28 @@ download of step n is issued at the start of step n+1 (or by `wait()`).  On
 one GPU the three copy/compute programs (first step, steady step, final
 download) are captured once as CUDA graphs, so a step costs one graph
 launch of host time.  Results are bitwise those of `advance_iteration`.
+
+Wavefront mode (round 2; one GPU, variants without work arrays -- SN, RA
+-- on grids of at least 64 planes; `wave_chunks` defaults to min(32,
+n0 / 16)): the step is cut into
+`wave_chunks` axis-0 plane chunks and the copies overlap the step's own
+compute as well.  Chunks are uploaded in ring order outward from chunk 0
+(0, 1, K-1, 2, K-2, ...), each one's primitives formed as it lands, and every
+stage of every chunk is launched (`fdns_stage_planes`, one compute stream)
+as soon as the chunks it reads are current: stage 1 of chunk c needs the
+uploads of c-1..c+1 (the padded ghost planes travel with the end chunks),
+stages 2 and 3 the previous stage on c-1..c+1 around the ring (their axis-0
+ghosts are the periodic images the other end's stage kernel wrote).  A
+chunk is downloaded once its third stage (and its neighbours', for the
+images) is done, and the next step's upload of a chunk waits only for that
+download.  Both link directions then stay busy across steps and the ~28 ms
+of compute of a 512^3 SN step hides under the copies: 173.5 -> 130.6 ms per
+step at 512^3 (K = 32), against 113 ms for 5.5 GB each way at the measured
+97 GB/s two-way PCIe aggregate (`tools/pcie_bidir.py`,
+`profiles/r02_e2e_wavefront.txt`).  Steps are
+enqueued eagerly (CUDA events between the copy and compute streams; a
+graph could not wait on the previous step's downloads).  Same kernels on
+plane ranges, so the same bits.
 """
 
 from __future__ import annotations
@@ -46,7 +68,8 @@ class HostStepper:
 
     def __init__(self, state: ConservativeState, evaluator: ResidualEvaluator,
                  scheme: RKScheme, host, chunks: int = 5,
-                 graphs: bool | None = None, upload: str = "ce"):
+                 graphs: bool | None = None, upload: str = "ce",
+                 wavefront: bool | None = None, wave_chunks: int | None = None):
         """`host`: a pinned float64 (5, padded...) tensor
         (`pinned_buffers`), or the reference's own five padded numpy arrays
         (rho, rhou0, rhou1, rhou2, rhoE as `Field.data` holds them), which
@@ -104,6 +127,17 @@ class HostStepper:
         self.use_graphs = single if graphs is None else graphs
         self._graphs = None
         self._pending = False   # the last step's result is not downloaded yet
+        n0 = state.grid.local_npoints[0]
+        if wave_chunks is None:     # 16-plane chunks, at most 32 (e2e A/B at
+            wave_chunks = min(32, n0 // 16)   # 512^3: K=8/16/32 -> 151/136/131 ms)
+        can_wave = (single and evaluator.work is None and scheme.stages == 3
+                    and upload == "ce" and wave_chunks >= 4 and n0 >= 8 * wave_chunks)
+        if wavefront and not can_wave:
+            raise ValueError("wavefront stepping needs one GPU, a variant without "
+                             "work arrays and >= 8 planes per chunk")
+        self.wavefront = can_wave if wavefront is None else bool(wavefront)
+        if self.wavefront:
+            self._wave_setup(wave_chunks)
 
     @staticmethod
     def pinned_buffers(grid) -> torch.Tensor:
@@ -179,13 +213,118 @@ class HostStepper:
         torch.cuda.synchronize()
         self._graphs = graphs
 
+    # -- wavefront mode ----------------------------------------------------
+    def _wave_setup(self, K: int) -> None:
+        g = self.state.grid
+        h, n0 = g.halo, g.local_npoints[0]
+        P0 = n0 + 2 * h
+        a = [n0 * c // K for c in range(K + 1)]            # interior plane cuts
+        self._wK = K
+        self._wi = [(a[c], a[c + 1]) for c in range(K)]    # interior planes
+        self._wp = [(0 if c == 0 else a[c] + h, P0 if c == K - 1 else a[c + 1] + h)
+                    for c in range(K)]                      # padded planes copied
+        order = [0]
+        for d in range(1, K // 2 + 1):
+            for c in (d, K - d):
+                if c not in order:
+                    order.append(c)
+        self._worder = order
+        # the compute sequence (chunk-stage launches in dependency order,
+        # interleaved with the primitives of each upload as it lands) and,
+        # per chunk, the stage-3 launches its download waits for
+        seq, up, done = [], set(), {1: set(), 2: set(), 3: set()}
+        ring = lambda c: {(c - 1) % K, c, (c + 1) % K}            # noqa: E731
+        line = lambda c: {x for x in (c - 1, c, c + 1) if 0 <= x < K}  # noqa: E731
+        for c in order:
+            seq.append(("P", c))
+            up.add(c)
+            progress = True
+            while progress:
+                progress = False
+                for sg in (1, 2, 3):
+                    for x in order:
+                        if x in done[sg]:
+                            continue
+                        need = line(x) <= up if sg == 1 else ring(x) <= done[sg - 1]
+                        if need:
+                            seq.append(("S", sg, x))
+                            done[sg].add(x)
+                            progress = True
+        assert all(len(done[sg]) == K for sg in (1, 2, 3))
+        self._wseq = seq
+        self._wdl_needs = {c: ring(c) for c in range(K)}
+        self._wev_dl = [None] * K       # previous step's download of each chunk
+        self._lib_w = _lib.load()
+
+    def _wave_step(self) -> None:
+        K, X = self._wK, self.state.bundle
+        Y, Z = self.ev.workspace()
+        src, dst = (X, Y, Z), (Y, Z, X)
+        main = torch.cuda.current_stream()
+        start = torch.cuda.Event()
+        start.record(main)
+        self.h2d.wait_event(start)
+        self.d2h.wait_event(start)
+        ev_up = {}
+        for c in self._worder:                      # uploads, ring order
+            if self._wev_dl[c] is not None:
+                self.h2d.wait_event(self._wev_dl[c])
+            lo, hi = self._wp[c]
+            with torch.cuda.stream(self.h2d):
+                for f in range(5):
+                    X[f, lo:hi].copy_(self._host_fields[f][lo:hi], non_blocking=True)
+            ev_up[c] = torch.cuda.Event()
+            ev_up[c].record(self.h2d)
+        problem, lib = self.ev.problem, self._lib_w
+        ev_s3 = {}
+        for item in self._wseq:                     # compute, one stream
+            if item[0] == "P":
+                c = item[1]
+                main.wait_event(ev_up[c])
+                lo, hi = self._wp[c]
+                _lib.check(lib.fdns_primitives_planes(_lib.ptr(X), lo, hi, problem,
+                                                      _lib.stream_handle()),
+                           "chunk primitives")
+                continue
+            _, sg, c = item
+            coef = self.scheme.alpha[sg - 1] * self.scheme.dt
+            i_lo, i_hi = self._wi[c]
+            self.ev.stage_planes(src[sg - 1], X, dst[sg - 1], coef, i_lo, i_hi, False)
+            if sg == 3:
+                ev_s3[c] = torch.cuda.Event()
+                ev_s3[c].record(main)
+        # downloads, in the order the chunks' neighbourhoods finish stage 3
+        done3, queued = set(), set()
+        for item in self._wseq:
+            if item[0] != "S" or item[1] != 3:
+                continue
+            done3.add(item[2])
+            for c in self._worder:
+                if c in queued or not self._wdl_needs[c] <= done3:
+                    continue
+                queued.add(c)
+                for x in self._wdl_needs[c]:
+                    self.d2h.wait_event(ev_s3[x])
+                lo, hi = self._wp[c]
+                with torch.cuda.stream(self.d2h):
+                    for f in range(5):
+                        self._host_fields[f][lo:hi].copy_(X[f, lo:hi], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(self.d2h)
+                self._wev_dl[c] = e
+        self.it.state.prim_source = Z
+
     # -- public ------------------------------------------------------------
     def step(self) -> None:
         """Upload the host fields, advance one RK3 iteration; the previous
         step's result is downloaded first, chunk by chunk, as the uploads
-        proceed."""
-        self._run("mid" if self._pending else "first")
-        self._pending = True
+        proceed (wavefront mode: this step's result is downloaded chunk by
+        chunk as its stages complete)."""
+        if self.wavefront:
+            self._wave_step()
+        else:
+            self._run("mid" if self._pending else "first")
+            self._pending = True
         self.it.time += self.scheme.dt
         self.it.iteration += 1
 
@@ -202,6 +341,9 @@ class HostStepper:
     def wait(self) -> None:
         """Download the last step's result into the host buffer; the buffer
         is complete once the current stream is synchronised."""
+        if self.wavefront:
+            torch.cuda.current_stream().wait_stream(self.d2h)
+            return
         if self._pending:
             self._run("last")
             self._pending = False

@@ -954,6 +954,49 @@ def test_host_stepper_matches_run(variant, graphs, chunks):
     assert stepper.it.iteration == 5
 
 
+@pytest.mark.parametrize("variant", ["SN", "RA"])
+@pytest.mark.parametrize("npts,k", [((40, 20, 24), 4), ((44, 16, 36), 5)])
+def test_host_stepper_wavefront_matches_run(variant, npts, k):
+    """Wavefront HostStepper (per-chunk uploads, primitives, stage launches
+    and downloads overlapped across the link directions and the compute
+    stream): the host arrays end up holding run()'s result bitwise, across a
+    wait() in the middle of the run and a host edit before the next step."""
+    from paper_1610_09146_b200.hostio import HostStepper
+    g = grid_of(npts)
+    F = npo.manufactured(npts, CO)
+    ref = state_from_cons(g, npo.interior(F[:5], 2))
+    fd.run(ref, fd.RKScheme(dt=2e-3), fd.ResidualEvaluator(g, C, variant), 2)
+    mid = ref.bundle[:5].cpu().numpy().copy()
+    fd.run(ref, fd.RKScheme(dt=2e-3), fd.ResidualEvaluator(g, C, variant), 3)
+    st = state_from_cons(g, npo.interior(F[:5], 2))
+    host = HostStepper.pinned_buffers(g)
+    host.copy_(st.bundle[:5].cpu())
+    stepper = HostStepper(st, fd.ResidualEvaluator(g, C, variant), fd.RKScheme(dt=2e-3),
+                          host, wavefront=True, wave_chunks=k)
+    assert stepper.wavefront
+    for _ in range(2):
+        stepper.step()
+    stepper.wait()
+    torch.cuda.synchronize()
+    assert np.array_equal(host.numpy(), mid)
+    for _ in range(3):
+        stepper.step()
+    stepper.wait()
+    torch.cuda.synchronize()
+    assert np.array_equal(host.numpy(), ref.bundle[:5].cpu().numpy())
+    # a host edit between wait() and step() is what the next step advances
+    edited = host.clone()
+    edited[0, 5:9] *= 1.001
+    host.copy_(edited)
+    st2 = state_from_cons(g, npo.interior(F[:5], 2))
+    st2.bundle[:5].copy_(edited.cuda())
+    fd.run(st2, fd.RKScheme(dt=2e-3), fd.ResidualEvaluator(g, C, variant), 1)
+    stepper.step()
+    stepper.wait()
+    torch.cuda.synchronize()
+    assert np.array_equal(host.numpy(), st2.bundle[:5].cpu().numpy())
+
+
 def test_host_stepper_on_reference_numpy_arrays():
     """HostStepper over five plain padded numpy arrays (the reference's own
     Field.data layout), page-locked in place: the arrays end up holding the
