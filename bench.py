@@ -544,17 +544,27 @@ def bench_e2e(fd, variant, grid, cons_host, steps):
         sec = float(t[0])
     npts = float(np.prod(grid.npoints))
     nbytes = host.numel() * 8
+    wave = getattr(stepper, "wavefront", False)
+    kw = getattr(stepper, "_wK", None)
     stepper.close() if hasattr(stepper, "close") else None
     del stepper, state, ev, host
     torch.cuda.empty_cache()
     return {"value": npts * 3 * steps / sec, "unit": UNIT,
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
             "steps": steps, "variant": variant,
-            "path": "hostio.HostStepper: pinned host fields -> advance one "
-                    "RK3 iteration -> host; field copies in chunks, each "
-                    "upload chunk right behind the previous result's "
-                    f"download of it ({E2E_CHUNKS} chunks/field), CUDA graphs"
-                    + ("; per rank: its slab" if multi else "")}
+            "path": ("hostio.HostStepper: pinned host fields -> advance one "
+                     "RK3 iteration -> host" + (
+                         f"; wavefront mode: {kw} axis-0 plane chunks, each "
+                         "uploaded in ring order, its primitives and every "
+                         "stage launched as soon as the chunks it reads are "
+                         "current, downloaded as its stage 3 completes; the "
+                         "next step's upload of a chunk waits only for its "
+                         "download (both PCIe directions and the compute "
+                         "overlap)" if wave else
+                         "; field copies in chunks, each upload chunk right "
+                         "behind the previous result's download of it "
+                         f"({E2E_CHUNKS} chunks/field), CUDA graphs")
+                     + ("; per rank: its slab" if multi else ""))}
 
 
 def variant_roofline(v, rec, fp64_tf, hbm_peak, hbm_src, n, fp64_sus=None, sms=148):

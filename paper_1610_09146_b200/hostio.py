@@ -22,7 +22,7 @@ download) are captured once as CUDA graphs, so a step costs one graph
 launch of host time.  Results are bitwise those of `advance_iteration`.
 
 Wavefront mode (round 2; one GPU, variants without work arrays -- SN, RA
--- on grids of at least 64 planes; `wave_chunks` defaults to min(32,
+-- on grids of at least 128 planes; `wave_chunks` defaults to min(32,
 n0 / 16)): the step is cut into
 `wave_chunks` axis-0 plane chunks and the copies overlap the step's own
 compute as well.  Chunks are uploaded in ring order outward from chunk 0
@@ -131,8 +131,10 @@ class HostStepper:
         if wave_chunks is None:     # 16-plane chunks, at most 32 (e2e A/B at
             wave_chunks = min(32, n0 // 16)   # 512^3: K=8/16/32 -> 151/136/131 ms)
         can_wave = (single and evaluator.work is None and scheme.stages == 3
-                    and upload == "ce" and wave_chunks >= 4 and n0 >= 8 * wave_chunks)
-        if wavefront and not can_wave:
+                    and upload == "ce" and wave_chunks >= 8 and n0 >= 8 * wave_chunks)
+        if wavefront and not (single and evaluator.work is None and scheme.stages == 3
+                              and upload == "ce" and wave_chunks >= 2
+                              and n0 >= 8 * wave_chunks):
             raise ValueError("wavefront stepping needs one GPU, a variant without "
                              "work arrays and >= 8 planes per chunk")
         self.wavefront = can_wave if wavefront is None else bool(wavefront)
