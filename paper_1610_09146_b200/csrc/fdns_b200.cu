@@ -747,6 +747,22 @@ inline dim3 point_grid(const Geom& g, dim3 blk) {
 // staged plane (TK+4, TJ+4, 1, 10).  Needs an even padded row (16-byte row
 // pitch); otherwise the point kernels run.
 // ---------------------------------------------------------------------------
+// L2 sector promotion of every TMA box load: 64 B (round 2).  A box row is
+// 36 or 32 doubles starting 16 B past a 32 B boundary (the padded row pitch
+// is (n2 + 4) * 8 B), so 256 B promotion pulled up to 2.7x each row's bytes
+// from DRAM: SN's stage reads 31.4 GB at 512^3 with 256 B, 28.4 with none,
+// 25.5 with 64 B; whole steps SN +1.7%, SS +0.5%, RA equal
+// (profiles/r02_l2_promotion_ab.txt).  A/B: FDNS_L2_PROMO = 0, 64, 128, 256.
+inline CUtensorMapL2promotion l2_promotion() {
+  static const int v = std::getenv("FDNS_L2_PROMO") ? std::atoi(std::getenv("FDNS_L2_PROMO")) : 64;
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 128: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static bool tried = false;
@@ -777,7 +793,7 @@ bool grad_map(CUtensorMap* m, const double* work, const Geom& g) {
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(work), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -796,7 +812,7 @@ bool grad_prefetch_map(CUtensorMap* m, const double* work, const Geom& g) {
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(work), dims,
                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -815,7 +831,7 @@ bool plane_map(CUtensorMap* m, const double* base, const Geom& g, int box_j = ti
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -834,7 +850,7 @@ bool saved_map(CUtensorMap* m, const double* saved, const Geom& g, int box_j = t
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(saved), dims,
                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -854,7 +870,7 @@ bool box_map(CUtensorMap* m, const double* base, const Geom& g, int nf, int64_t 
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims,
                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
