@@ -438,13 +438,24 @@ __device__ __forceinline__ double energy_suffix(const Coef& k, const Pv& P, cons
 }
 
 // RHOE_INTERNAL: r[RHOE_F] already holds rho*e (staged-tile accessors).
-template <bool RHOE_INTERNAL = false, class Pv>
+// MOMENTUM_FIRST: evaluate the momentum equations before mass and energy
+// (each equation's own association is unchanged, so the bits are too); the
+// 12-warp SN kernel schedules ~1% faster that way at 512^3, the other
+// variants do not gain (profiles/r02_residual_order_ab.txt).
+template <bool RHOE_INTERNAL = false, bool MOMENTUM_FIRST = false, class Pv>
 __device__ __forceinline__ void residual_point(const Coef& k, const Pv& P, const double* r,
                                                double* out) {
-  out[0] = mass_residual(k, P, r);
-  out[1] = momentum<0>(k, P, r);
-  out[2] = momentum<1>(k, P, r);
-  out[3] = momentum<2>(k, P, r);
+  if constexpr (MOMENTUM_FIRST) {
+    out[1] = momentum<0>(k, P, r);
+    out[2] = momentum<1>(k, P, r);
+    out[3] = momentum<2>(k, P, r);
+    out[0] = mass_residual(k, P, r);
+  } else {
+    out[0] = mass_residual(k, P, r);
+    out[1] = momentum<0>(k, P, r);
+    out[2] = momentum<1>(k, P, r);
+    out[3] = momentum<2>(k, P, r);
+  }
   out[4] = energy_suffix(k, P, r, energy_prefix<RHOE_INTERNAL>(k, P, r));
 }
 #undef G

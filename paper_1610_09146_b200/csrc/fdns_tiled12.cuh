@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
       } else {
         const tiled::TiledLazyProviderT<SAcc12, TK> P{
             k, a, q1, q2, bufs + toff, bu1 + toff, bu2 + (tj + 2) * TK + tk};
-        residual_point<true>(k, P, r, R);
+        residual_point<true, true>(k, P, r, R);
       }
       if (active) {
         if constexpr (MODE == 0) {
