@@ -997,6 +997,32 @@ def test_host_stepper_wavefront_matches_run(variant, npts, k):
     assert np.array_equal(host.numpy(), st2.bundle[:5].cpu().numpy())
 
 
+def test_host_stepper_wavefront_is_the_default_from_128_planes():
+    """The bench's e2e path: the stepper picks the wavefront by itself for SN
+    on one GPU from 128 planes (8 chunks here) and stays bitwise equal to
+    run()."""
+    from paper_1610_09146_b200.hostio import HostStepper
+    npts = (128, 12, 16)
+    g = grid_of(npts)
+    F = npo.manufactured(npts, CO)
+    ref = state_from_cons(g, npo.interior(F[:5], 2))
+    fd.run(ref, fd.RKScheme(dt=2e-3), fd.ResidualEvaluator(g, C, "SN"), 3)
+    st = state_from_cons(g, npo.interior(F[:5], 2))
+    host = HostStepper.pinned_buffers(g)
+    host.copy_(st.bundle[:5].cpu())
+    stepper = HostStepper(st, fd.ResidualEvaluator(g, C, "SN"), fd.RKScheme(dt=2e-3), host)
+    assert stepper.wavefront and stepper._wK == 8
+    for _ in range(3):
+        stepper.step()
+    stepper.wait()
+    torch.cuda.synchronize()
+    assert np.array_equal(host.numpy(), ref.bundle[:5].cpu().numpy())
+    # variants with work arrays keep the whole-step pipeline
+    other = HostStepper(state_from_cons(g, npo.interior(F[:5], 2)),
+                        fd.ResidualEvaluator(g, C, "SS"), fd.RKScheme(dt=2e-3), host)
+    assert not other.wavefront
+
+
 def test_host_stepper_on_reference_numpy_arrays():
     """HostStepper over five plain padded numpy arrays (the reference's own
     Field.data layout), page-locked in place: the arrays end up holding the
