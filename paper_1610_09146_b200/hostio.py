@@ -58,6 +58,49 @@ from .timeloop import IterationState, RKScheme, _fused_iteration
 UPLOAD_CTAS = 296
 
 
+def wave_schedule(n0: int, h: int, K: int) -> dict:
+    """The wavefront step's plan for n0 interior planes (halo h) in K chunks:
+    interior and padded plane ranges per chunk (the end chunks carry the
+    padded ghost planes), the upload order (ring distance from chunk 0),
+    the compute sequence -- ("P", c) primitives of an uploaded chunk,
+    ("S", stage, c) a stage of a chunk, each as soon as what it reads is
+    current: stage 1 the uploads of c-1..c+1 (no wrap: the ghosts travel
+    with the end chunks), stages 2-3 the previous stage on c-1..c+1 around
+    the ring (their axis-0 ghosts are the images the far end wrote) -- and
+    the stage-3 chunks each download waits for (itself and its ring
+    neighbours, whose images land in its ghost planes)."""
+    P0 = n0 + 2 * h
+    a = [n0 * c // K for c in range(K + 1)]
+    interior = [(a[c], a[c + 1]) for c in range(K)]
+    padded = [(0 if c == 0 else a[c] + h, P0 if c == K - 1 else a[c + 1] + h)
+              for c in range(K)]
+    order = [0]
+    for d in range(1, K // 2 + 1):
+        for c in (d, K - d):
+            if c not in order:
+                order.append(c)
+    ring = lambda c: {(c - 1) % K, c, (c + 1) % K}            # noqa: E731
+    line = lambda c: {x for x in (c - 1, c, c + 1) if 0 <= x < K}  # noqa: E731
+    seq, up, done = [], set(), {1: set(), 2: set(), 3: set()}
+    for c in order:
+        seq.append(("P", c))
+        up.add(c)
+        progress = True
+        while progress:
+            progress = False
+            for sg in (1, 2, 3):
+                for x in order:
+                    if x in done[sg]:
+                        continue
+                    if (line(x) <= up) if sg == 1 else (ring(x) <= done[sg - 1]):
+                        seq.append(("S", sg, x))
+                        done[sg].add(x)
+                        progress = True
+    assert all(len(done[sg]) == K for sg in (1, 2, 3))
+    return {"interior": interior, "padded": padded, "order": order, "seq": seq,
+            "download_needs": {c: ring(c) for c in range(K)}}
+
+
 class HostStepper:
     """Advance a host-resident conservative state on the GPU, one RK3
     iteration per `step`, with pipelined host<->device copies.
@@ -218,43 +261,11 @@ class HostStepper:
     # -- wavefront mode ----------------------------------------------------
     def _wave_setup(self, K: int) -> None:
         g = self.state.grid
-        h, n0 = g.halo, g.local_npoints[0]
-        P0 = n0 + 2 * h
-        a = [n0 * c // K for c in range(K + 1)]            # interior plane cuts
+        sched = wave_schedule(g.local_npoints[0], g.halo, K)
         self._wK = K
-        self._wi = [(a[c], a[c + 1]) for c in range(K)]    # interior planes
-        self._wp = [(0 if c == 0 else a[c] + h, P0 if c == K - 1 else a[c + 1] + h)
-                    for c in range(K)]                      # padded planes copied
-        order = [0]
-        for d in range(1, K // 2 + 1):
-            for c in (d, K - d):
-                if c not in order:
-                    order.append(c)
-        self._worder = order
-        # the compute sequence (chunk-stage launches in dependency order,
-        # interleaved with the primitives of each upload as it lands) and,
-        # per chunk, the stage-3 launches its download waits for
-        seq, up, done = [], set(), {1: set(), 2: set(), 3: set()}
-        ring = lambda c: {(c - 1) % K, c, (c + 1) % K}            # noqa: E731
-        line = lambda c: {x for x in (c - 1, c, c + 1) if 0 <= x < K}  # noqa: E731
-        for c in order:
-            seq.append(("P", c))
-            up.add(c)
-            progress = True
-            while progress:
-                progress = False
-                for sg in (1, 2, 3):
-                    for x in order:
-                        if x in done[sg]:
-                            continue
-                        need = line(x) <= up if sg == 1 else ring(x) <= done[sg - 1]
-                        if need:
-                            seq.append(("S", sg, x))
-                            done[sg].add(x)
-                            progress = True
-        assert all(len(done[sg]) == K for sg in (1, 2, 3))
-        self._wseq = seq
-        self._wdl_needs = {c: ring(c) for c in range(K)}
+        self._wi, self._wp = sched["interior"], sched["padded"]
+        self._worder, self._wseq = sched["order"], sched["seq"]
+        self._wdl_needs = sched["download_needs"]
         self._wev_dl = [None] * K       # previous step's download of each chunk
         self._lib_w = _lib.load()
 

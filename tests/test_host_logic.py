@@ -305,3 +305,43 @@ def test_decompose_workers_and_scaling_drivers():
                                     (64, 64, 32), (64, 64, 64)]
     assert all(r.ideal == 1.0 for r in wk)
     assert [r.normalized for r in wk] == pytest.approx([1, 1, 1, 1])
+
+
+@pytest.mark.parametrize("n0,K", [(512, 32), (128, 8), (44, 5), (40, 4), (257, 16)])
+def test_wave_schedule_is_a_valid_order(n0, K):
+    """hostio.wave_schedule (the e2e wavefront): every chunk's primitives
+    and three stages appear once, each after what it reads (stage 1: the
+    primitives of c-1..c+1 without wrap, whose planes include the ghosts;
+    stages 2-3: the previous stage on c-1..c+1 around the ring); chunk
+    ranges tile the interior and the padded planes exactly."""
+    from paper_1610_09146_b200.hostio import wave_schedule
+    h = 2
+    s = wave_schedule(n0, h, K)
+    assert sorted(s["order"]) == list(range(K))
+    it = s["interior"]
+    assert it[0][0] == 0 and it[-1][1] == n0
+    assert all(it[c][1] == it[c + 1][0] and it[c][1] - it[c][0] >= n0 // K for c in range(K - 1))
+    pd = s["padded"]
+    assert pd[0][0] == 0 and pd[-1][1] == n0 + 2 * h
+    assert all(pd[c][1] == pd[c + 1][0] for c in range(K - 1))
+    assert all(pd[c] == (it[c][0] + h, it[c][1] + h) for c in range(1, K - 1))
+    seen = set()
+    for item in s["seq"]:
+        assert item not in seen
+        if item[0] == "S":
+            _, sg, c = item
+            if sg == 1:
+                need = {("P", x) for x in (c - 1, c, c + 1) if 0 <= x < K}
+            else:
+                need = {("S", sg - 1, x % K) for x in (c - 1, c, c + 1)}
+            assert need <= seen, (item, need - seen)
+        seen.add(item)
+    assert seen == {("P", c) for c in range(K)} | {
+        ("S", sg, c) for sg in (1, 2, 3) for c in range(K)}
+    assert s["download_needs"][0] == {K - 1, 0, 1 % K}
+    # the first chunk's third stage comes before the last upload: the
+    # downloads start while uploads are still running
+    first_s3 = next(i for i, x in enumerate(s["seq"]) if x[:2] == ("S", 3))
+    last_p = max(i for i, x in enumerate(s["seq"]) if x[0] == "P")
+    if K >= 8:
+        assert first_s3 < last_p
