@@ -186,6 +186,13 @@ int32_t fdns_l2_flush(void* buf, int64_t bytes, void* stream);
  * plan.py:394-416). */
 int32_t fdns_copy_sm(void* dst, const void* src, int64_t bytes, int32_t ctas, void* stream);
 
+/* `rows` runs of `row_bytes` each, `src_pitch` / `dst_pitch` bytes apart,
+ * copied by a copy engine (cudaMemcpy2DAsync, direction inferred from the
+ * pointers): one DMA operation for the same plane range of several fields
+ * of a bundle (hostio.py's chunk uploads and downloads). */
+int32_t fdns_copy_rows(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                       int64_t row_bytes, int64_t rows, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,8 @@ EXPORTS = {
     "fdns_fp64_probe": (_I, [_VP, _I, _D, _VP]),
     "fdns_l2_flush": (_I, [_VP, ctypes.c_int64, _VP]),
     "fdns_copy_sm": (_I, [_VP, _VP, ctypes.c_int64, _I, _VP]),
+    "fdns_copy_rows": (_I, [_VP, ctypes.c_int64, _VP, ctypes.c_int64, ctypes.c_int64,
+                            ctypes.c_int64, _VP]),
     "fdns_derivative": (_I, [_VP, _VP, _I, ctypes.POINTER(Problem), _VP]),
 }
 

@@ -1618,6 +1618,16 @@ int32_t fdns_l2_flush(void* buf, int64_t bytes, void* stream) {
   return check_launch("l2 flush");
 }
 
+int32_t fdns_copy_rows(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch,
+                       int64_t row_bytes, int64_t rows, void* stream) {
+  if (rows <= 0 || row_bytes <= 0) return 0;
+  const cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)dst_pitch, src, (size_t)src_pitch,
+                                          (size_t)row_bytes, (size_t)rows, cudaMemcpyDefault,
+                                          (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail("fdns_copy_rows", e);
+  return 0;
+}
+
 int32_t fdns_copy_sm(void* dst, const void* src, int64_t bytes, int32_t ctas, void* stream) {
   if (((uintptr_t)dst | (uintptr_t)src | (uintptr_t)bytes) & 15)
     return fail("fdns_copy_sm: pointers and size must be 16-byte aligned");

@@ -35,9 +35,10 @@ ghosts are the periodic images the other end's stage kernel wrote).  A
 chunk is downloaded once its third stage (and its neighbours', for the
 images) is done, and the next step's upload of a chunk waits only for that
 download.  Both link directions then stay busy across steps and the ~28 ms
-of compute of a 512^3 SN step hides under the copies: 173.5 -> 130.6 ms per
-step at 512^3 (K = 32), against 113 ms for 5.5 GB each way at the measured
-97 GB/s two-way PCIe aggregate (`tools/pcie_bidir.py`,
+of compute of a 512^3 SN step hides under the copies: 162-173 -> 118 ms per
+step at 512^3 (K = 32; a chunk is one 2-D copy-engine operation over the
+five fields, `fdns_copy_rows`), against 113 ms for 5.5 GB each way at the
+measured 97 GB/s two-way PCIe aggregate (`tools/pcie_bidir.py`,
 `profiles/r02_e2e_wavefront.txt`).  Steps are
 enqueued eagerly (CUDA events between the copy and compute streams; a
 graph could not wait on the previous step's downloads).  Same kernels on
@@ -269,6 +270,24 @@ class HostStepper:
         self._wev_dl = [None] * K       # previous step's download of each chunk
         self._lib_w = _lib.load()
 
+    def _copy_chunk(self, X, host_fields, lo: int, hi: int, upload: bool) -> None:
+        """Planes [lo, hi) of the five conservative fields, one copy-engine
+        operation when the host side is one pinned block (five rows of a
+        2-D copy, a field apart), else one copy per field."""
+        if isinstance(self.host, torch.Tensor):
+            plane = X.stride(1) * 8
+            dev, hst = X[0, lo].data_ptr(), self.host[0, lo].data_ptr()
+            dst, src = (dev, hst) if upload else (hst, dev)
+            _lib.check(self._lib_w.fdns_copy_rows(
+                dst, X.stride(0) * 8, src, self.host.stride(0) * 8,
+                (hi - lo) * plane, 5, _lib.stream_handle()), "chunk copy")
+            return
+        for f in range(5):
+            if upload:
+                X[f, lo:hi].copy_(host_fields[f][lo:hi], non_blocking=True)
+            else:
+                host_fields[f][lo:hi].copy_(X[f, lo:hi], non_blocking=True)
+
     def _wave_step(self) -> None:
         K, X = self._wK, self.state.bundle
         Y, Z = self.ev.workspace()
@@ -284,8 +303,7 @@ class HostStepper:
                 self.h2d.wait_event(self._wev_dl[c])
             lo, hi = self._wp[c]
             with torch.cuda.stream(self.h2d):
-                for f in range(5):
-                    X[f, lo:hi].copy_(self._host_fields[f][lo:hi], non_blocking=True)
+                self._copy_chunk(X, self._host_fields, lo, hi, upload=True)
             ev_up[c] = torch.cuda.Event()
             ev_up[c].record(self.h2d)
         problem, lib = self.ev.problem, self._lib_w
@@ -320,8 +338,7 @@ class HostStepper:
                     self.d2h.wait_event(ev_s3[x])
                 lo, hi = self._wp[c]
                 with torch.cuda.stream(self.d2h):
-                    for f in range(5):
-                        self._host_fields[f][lo:hi].copy_(X[f, lo:hi], non_blocking=True)
+                    self._copy_chunk(X, self._host_fields, lo, hi, upload=False)
                 e = torch.cuda.Event()
                 e.record(self.d2h)
                 self._wev_dl[c] = e
