@@ -427,59 +427,6 @@ __global__ void __launch_bounds__(MARCH_NT, FDNS_MARCH_SMEM_MINB) k_fill_bl_marc
   }
 }
 
-// SS/RS: the nine velocity gradients (u0..u2 queued; queue slot q = field
-// U0 + q, remapped by QAccU below).
-struct QAccU {   // (E_FIELD taps only: no kInternalEnergy needed)
-  const double (&q)[3][5];
-  const double* __restrict__ b;
-  int64_t c, s0, s1, fs;
-  __device__ __forceinline__ double v(int f, int di, int dj, int dk) const {
-    if (dj == 0 && dk == 0) return q[f - U0][di + 2];
-    return __ldg(b + f * fs + c + di * s0 + dj * s1 + dk);
-  }
-};
-
-template <int NPL>
-__global__ void __launch_bounds__(MARCH_BX * MARCH_BY) k_grad_ss_march(
-    const double* __restrict__ in, double* __restrict__ ws, Coef k, Geom g) {
-  pdl_entry();
-  const int kk = point_k(g);
-  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
-  if (kk < 0 || kk >= g.n2 || jj >= g.n1) return;
-  const int i0 = blockIdx.z * NPL, i1 = min(i0 + NPL, g.n0);
-  const int64_t col = (int64_t)(jj + g.h) * g.s1 + (kk + g.h);
-  constexpr int fld[3] = {U0, U1, U2};
-  double q[3][5], nx[3];
-#pragma unroll
-  for (int d = 0; d < 4; ++d) {
-    double t[3];
-    load_plane<3>(t, in, (int64_t)(i0 - 2 + d + g.h) * g.s0 + col, g.fs, fld);
-#pragma unroll
-    for (int f = 0; f < 3; ++f) q[f][d] = t[f];
-  }
-  load_plane<3>(nx, in, (int64_t)(i0 + 2 + g.h) * g.s0 + col, g.fs, fld);
-#pragma unroll 1
-  for (int i = i0; i < i1; ++i) {
-#pragma unroll
-    for (int f = 0; f < 3; ++f) q[f][4] = nx[f];
-    if (i + 1 < i1) load_plane<3>(nx, in, (int64_t)(i + 3 + g.h) * g.s0 + col, g.fs, fld);
-    const int64_t c = (int64_t)(i + g.h) * g.s0 + col;
-    const QAccU a{q, in, c, g.s0, g.s1, g.fs};
-    ws[(0 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U0, 0>(k, a);
-    ws[(0 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U0, 0>(k, a);
-    ws[(0 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U0, 0>(k, a);
-    ws[(1 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U1, 0>(k, a);
-    ws[(1 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U1, 0>(k, a);
-    ws[(1 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U1, 0>(k, a);
-    ws[(2 * 3 + 0) * g.fs + c] = d1<0, E_FIELD, U2, 0>(k, a);
-    ws[(2 * 3 + 1) * g.fs + c] = d1<1, E_FIELD, U2, 0>(k, a);
-    ws[(2 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U2, 0>(k, a);
-#pragma unroll
-    for (int f = 0; f < 3; ++f)
-#pragma unroll
-      for (int d = 0; d < 4; ++d) q[f][d] = q[f][d + 1];
-  }
-}
 
 // D(u_Q, x_Q) on the ghost frame only: points whose axis-Q coordinate is
 // interior while another coordinate lies in the halo (the interior values
@@ -1315,7 +1262,6 @@ inline int march_fill_mode(const Geom& g) {
   if (g_march_fill >= 0) return g_march_fill;
   return (int64_t)g.n1 * g.n2 >= 384 * 384 ? 2 : 0;
 }
-const bool g_march_ss = std::getenv("FDNS_MARCH_SS") && std::atoi(std::getenv("FDNS_MARCH_SS")) == 1;
 // A/B switch: FDNS_SS_FILL_1D=1 selects the one-launch grid-stride SS fill.
 const bool g_ss_fill_3d = std::getenv("FDNS_SS_FILL_1D") == nullptr;
 
@@ -1373,10 +1319,7 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
   // frames (+6% SS/RS steps at 256^3); below, one grid-stride launch
   // (its single launch wins at 64^3: -4% otherwise)
   if ((variant == FDNS_SS || variant == FDNS_RS) && g_ss_fill_3d && g.n2 >= 128) {
-    if (g_march_ss && g.n0 >= 2 * MARCH_NPL)
-      k_grad_ss_march<MARCH_NPL><<<march_grid(MARCH_NPL), mblk, 0, s>>>(in, work, k, g);
-    else
-      k_grad_ss_interior<<<grd, blk, 0, s>>>(in, work, k, g);
+    k_grad_ss_interior<<<grd, blk, 0, s>>>(in, work, k, g);
     ghosts(work + 0 * g.fs, work + 4 * g.fs, work + 8 * g.fs, false);
     count(2);
     return check_launch("SS fills");
