@@ -27,9 +27,9 @@
 // split applies (see fdns_b200.cu:use_t12_ss): their buffer set is the three
 // TMA boxes of the centre plane's stored diagonal gradients; the axis-0
 // queues and the six off-diagonal gradients are per-thread loads, as in the
-// 8-warp kernel.  Whole RK3 steps at 512^3: SS +1.8-2.6%, RS +0.2-1.7%; at
-// 256^3 SS equal, RS -3%; without the round-robin split 6-11% slower (more
-// DRAM traffic; profiles/r02_ss_t12_ab.txt).  There is no shared memory left
+// 8-warp kernel.  Whole RK3 steps at 512^3 (interleaved A/B): SS +1.2-4.1%,
+// RS -2..+1.7%; at 256^3 SS equal, RS -3%; without the round-robin split
+// 6-11% slower (more DRAM traffic; profiles/r02_ss_t12_ab.txt).  There is no shared memory left
 // to stage the off-diagonal gradients, so its load/store unit is busier
 // than SN's (mio + lg throttle stalls ~0.8 vs ~0.4 cycles per instruction).
 //
@@ -38,7 +38,7 @@
 // and D(u1,x1), D(u2,x2) on plane i-2), so its buffer set holds, instead of
 // SN's centre-plane derivatives, plane i-2's u0 box, u1 rows and u2 columns,
 // copied before the step barrier (SAccRA12).  167 registers, no spills;
-// whole RK3 steps +6.6% / +3.9% / +6.3% over the 8-warp RA kernel at
+// whole RK3 steps +6.6% / +3.9% / +5.5-6.3% over the 8-warp RA kernel at
 // 128^3 / 256^3 / 512^3.  (A 32 x 10 tile on a 6-slot ring of nine fields,
 // 10 warps, was 7% slower than 8 warps: two of the four schedulers then
 // carry three warps and the step barrier waits for them.)
