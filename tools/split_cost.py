@@ -4,6 +4,8 @@ one fused stage over all planes vs the boundary-planes-first split that
 CUDA events, L2 flushed before each.
 
     python tools/split_cost.py --sizes 64,128 --variants SN,SS
+    python tools/split_cost.py --grids 512x512x512,64x512x512 --variants SN,RA,SS,BL
+      (a strong-scaling rank's slab of 512^3 on 8 GPUs as a one-GPU grid)
 """
 import argparse
 import os
@@ -34,13 +36,17 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default="64,128")
     ap.add_argument("--variants", default="SN,SS")
+    ap.add_argument("--grids", default="", help="n0xn1xn2,... (overrides --sizes)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     lib = _lib.load()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     c = fd.PhysicalConstants()
-    for n in map(int, a.sizes.split(",")):
-        g = fd.make_grid((n,) * 3, (2 * np.pi,) * 3)
+    shapes = ([tuple(map(int, x.split("x"))) for x in a.grids.split(",")] if a.grids
+              else [(n,) * 3 for n in map(int, a.sizes.split(","))])
+    for npts in shapes:
+        n = "x".join(map(str, npts))
+        g = fd.make_grid(npts, (2 * np.pi,) * 3)
         for v in a.variants.split(","):
             s = fd.taylor_green_init(g, c)
             ev = fd.ResidualEvaluator(g, c, v)
