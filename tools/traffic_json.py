@@ -52,9 +52,15 @@ def main():
     out = json.load(open(out_path)) if os.path.exists(out_path) else {}
     for v, rs in stages.items():
         dram = sum(val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum") for r in rs)
-        fp = sum(val(r, "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum") +
-                 val(r, "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum") +
-                 val(r, "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum") for r in rs)
+        def fp64(r):
+            ops = ("dadd", "dmul", "dfma")
+            tot = sum(val(r, f"smsp__sass_thread_inst_executed_op_{o}_pred_on.sum") for o in ops)
+            if tot == 0:   # captures that only hold the per-cycle rates
+                tot = sum(val(r, f"smsp__sass_thread_inst_executed_op_{o}_pred_on.sum."
+                                 "per_cycle_elapsed") for o in ops) * \
+                    val(r, "smsp__cycles_elapsed.avg")
+            return tot
+        fp = sum(fp64(r) for r in rs)
         kern = [r[ix["Kernel Name"]].split("(")[0].replace("void ", "") for r in rs]
         rec = {"dram_bytes": dram, "kernels": kern,
                "time_ms": sum(val(r, "gpu__time_duration.sum") for r in rs),
