@@ -1023,6 +1023,27 @@ def test_host_stepper_wavefront_is_the_default_from_128_planes():
     assert not other.wavefront
 
 
+def test_host_stepper_wavefront_on_reference_numpy_arrays():
+    """Wavefront stepping over the reference's own five padded numpy arrays
+    (page-locked in place; chunk copies per field): bitwise run()."""
+    from paper_1610_09146_b200.hostio import HostStepper
+    npts = (40, 20, 24)
+    g = grid_of(npts)
+    F = npo.manufactured(npts, CO)
+    ref = state_from_cons(g, npo.interior(F[:5], 2))
+    fd.run(ref, fd.RKScheme(dt=2e-3), fd.ResidualEvaluator(g, C, "SN"), 3)
+    st = state_from_cons(g, npo.interior(F[:5], 2))
+    arrays = [np.ascontiguousarray(a) for a in st.bundle[:5].cpu().numpy()]
+    stepper = HostStepper(st, fd.ResidualEvaluator(g, C, "SN"), fd.RKScheme(dt=2e-3),
+                          arrays, wavefront=True, wave_chunks=4)
+    for _ in range(3):
+        stepper.step()
+    stepper.wait()
+    torch.cuda.synchronize()
+    stepper.close()
+    assert np.array_equal(np.stack(arrays), ref.bundle[:5].cpu().numpy())
+
+
 def test_host_stepper_on_reference_numpy_arrays():
     """HostStepper over five plain padded numpy arrays (the reference's own
     Field.data layout), page-locked in place: the arrays end up holding the
