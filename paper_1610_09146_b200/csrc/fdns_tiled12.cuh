@@ -380,12 +380,18 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
         double* r1 = bufs + PLANE;             // u1, PJ x TK
         double* r2 = bufs + PLANE + BU2_N;     // u2, TJ x PK
         static_assert(BU2_N == L::PJ * TK && BU1_N == TJ * PK, "RA buffer shapes");
-#pragma unroll 1
-        for (int x0 = tid; x0 < PLANE; x0 += NT) bufs[x0] = old[U0 * PLANE + x0];
-#pragma unroll 1
-        for (int y = tid; y < BU2_N; y += NT) r1[y] = old[U1 * PLANE + (y / TK) * PK + 2 + y % TK];
-#pragma unroll 1
-        for (int y = tid; y < BU1_N; y += NT) r2[y] = old[U2 * PLANE + 2 * PK + y];
+        // each buffer's items past the first NT go to the highest thread
+        // ids: the arrival conversion gave its extra points to the lowest
+        // ones, so the pre-barrier work evens out across the warps
+        auto copy = [&](int n, auto&& item) {
+          item(tid);
+          const int x = tid + n - 2 * NT;   // items NT..n-1 -> tids 2NT-n..NT-1
+          if (x >= 0 && n > NT) item(x + NT);
+        };
+        static_assert(PLANE <= 2 * NT && BU2_N <= 2 * NT && BU1_N <= 2 * NT, "two items at most");
+        copy(PLANE, [&](int x0) { bufs[x0] = old[U0 * PLANE + x0]; });
+        copy(BU2_N, [&](int y) { r1[y] = old[U1 * PLANE + (y / TK) * PK + 2 + y % TK]; });
+        copy(BU1_N, [&](int y) { r2[y] = old[U2 * PLANE + 2 * PK + y]; });
       } else if constexpr (kGB) {
         // stored gradient boxes: TMA (issue_gb_tile)
       } else {
