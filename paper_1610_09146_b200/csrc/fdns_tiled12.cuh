@@ -184,6 +184,52 @@ __device__ __forceinline__ void stage_arrival(const Coef& k, double* slot, int t
   }
 }
 
+// Staggered arrival conversion (round 2, RA: kStagger).  A box has 576
+// points for 384 threads, so converting a whole plane per step gave half the
+// warps two points and the other half one, and every step barrier waited
+// for the first half.  But rho*e and T of a plane are only read at the
+// thread's own column until the plane becomes the centre plane (the
+// axis-0 taps), and in-plane around it then; so each step a thread converts
+// its own point of the newest plane in full, and the 192 halo points are
+// converted in two halves on the two following steps -- rho*e by threads
+// 0..191 one step after arrival, T (from that rho*e) by threads 192..383 on
+// the step the plane becomes the centre, before its barrier.  Same
+// expressions on the same values, so the same bits; every thread now does
+// one conversion plus half a halo conversion per step.
+// Measured (profiles/r02_stagger_ab.txt): RA +0.7%; SN 1.3-2.8% slower (one
+// more live register tips it into spills; its buffer computation already
+// evens the warps out), SS unchanged -- so RA only.
+template <class L>
+__device__ __forceinline__ int halo_pos(int h) {   // h in [0, 4 * (PK + TJ))
+  constexpr int PK = L::PK, PJ = L::PJ;
+  if (h < 2 * PK) return h;                          // rows 0, 1
+  h -= 2 * PK;
+  if (h < 2 * PK) return (PJ - 2) * PK + h;          // rows PJ-2, PJ-1
+  h -= 2 * PK;
+  const int row = 2 + h / 4, c = h % 4;              // columns 0, 1, PK-2, PK-1
+  return row * PK + (c < 2 ? c : PK - 4 + c);
+}
+template <class L>
+__device__ __forceinline__ void conv_e(const Coef& k, double* slot, int x) {
+  constexpr int PLANE = L::PLANE;
+  (void)k;
+  slot[RHOE_F * PLANE + x] = slot[RHOE_F * PLANE + x] -
+                             0.5 * (slot[RU0 * PLANE + x] * slot[U0 * PLANE + x] +
+                                    slot[RU1 * PLANE + x] * slot[U1 * PLANE + x] +
+                                    slot[RU2 * PLANE + x] * slot[U2 * PLANE + x]);
+}
+template <class L>
+__device__ __forceinline__ void conv_T(const Coef& k, double* slot, int x) {
+  constexpr int PLANE = L::PLANE;
+  const double p = k.gm1 * slot[RHOE_F * PLANE + x];
+  slot[SF_T * PLANE + x] = k.gM2 * p / slot[RHO * PLANE + x];
+}
+template <class L>
+__device__ __forceinline__ void conv_full(const Coef& k, double* slot, int x) {
+  conv_e<L>(k, slot, x);
+  conv_T<L>(k, slot, x);
+}
+
 // SS / RS: the three TMA boxes of the centre plane's stored diagonal
 // gradients, laid out like SN's buffer set: D(u0,x0) over the whole box,
 // D(u1,x1) over the tile rows (pitch PK), D(u2,x2) over the tile columns
@@ -203,6 +249,7 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
   static_assert(V == FDNS_SN || V == FDNS_RA || V == FDNS_SS || V == FDNS_RS,
                 "12-warp kernel variant");
   constexpr bool kGB = (V == FDNS_SS || V == FDNS_RS);
+  constexpr bool kStagger = (V == FDNS_RA && TJ_ == 12);   // staggered arrival conversion
   using L = Lay<TJ_>;
   constexpr int TK = L::TK, TJ = L::TJ, NT = L::NT, PK = L::PK, PLANE = L::PLANE;
   constexpr int SLOT = L::SLOT, BU1_N = L::BU1_N, BU2_N = L::BU2_N, BUFSET = L::BUFSET;
@@ -306,6 +353,7 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
     const int jj = j0 + tj, kk = k0 + tk;
     const bool active = jj < g.n1 && kk < g.n2;
     const int toff = (tj + 2) * PK + (tk + 2);
+    const int hx = halo_pos<L>(tid < NT / 2 ? tid : tid - NT / 2);   // staggered halo item
     const int nsteps = (int)(se - x);
     const int i_seg = i_lo + plane_at(x);
     double q1[5], q2[5];
@@ -356,7 +404,26 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
         gv[2 * 3 + 0] = __ldg(work + 6 * g.fs + cl);
         gv[2 * 3 + 1] = __ldg(work + 7 * g.fs + cl);
       }
-      if (t == 0) {
+      if constexpr (kStagger) {
+        static_assert(4 * (PK + TJ) == NT / 2, "halo points = half the threads");
+        if (t == 0) {
+          // a new window: own points of all five planes, the centre plane's
+          // halo in full (threads 0..191), the next plane's halo rho*e
+          // (threads 192..383); its T follows on the next step
+          for (int d = 0; d < 5; ++d) {
+            mbar_wait(&bars[slot_of(d)], ((w + d) / NR) & 1);
+            conv_full<L>(k, sm + slot_of(d) * SLOT, toff);
+          }
+          if (tid < NT / 2) conv_full<L>(k, sm + slot_of(2) * SLOT, hx);
+          else conv_e<L>(k, sm + slot_of(3) * SLOT, hx);
+          __syncthreads();   // halo values written by other threads
+        } else {
+          mbar_wait(&bars[slot_of(4)], ((w + 4) / NR) & 1);
+          conv_full<L>(k, sm + slot_of(4) * SLOT, toff);
+          if (tid < NT / 2) conv_e<L>(k, sm + slot_of(3) * SLOT, hx);
+          else conv_T<L>(k, sm + slot_of(2) * SLOT, hx);
+        }
+      } else if (t == 0) {
         for (int d = 0; d < 5; ++d) {
           mbar_wait(&bars[slot_of(d)], ((w + d) / NR) & 1);
           stage_arrival<L>(k, sm + slot_of(d) * SLOT, tid);
@@ -383,15 +450,31 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
         // each buffer's items past the first NT go to the highest thread
         // ids: the arrival conversion gave its extra points to the lowest
         // ones, so the pre-barrier work evens out across the warps
-        auto copy = [&](int n, auto&& item) {
-          item(tid);
-          const int x = tid + n - 2 * NT;   // items NT..n-1 -> tids 2NT-n..NT-1
-          if (x >= 0 && n > NT) item(x + NT);
-        };
+        auto cp0 = [&](int x0) { bufs[x0] = old[U0 * PLANE + x0]; };
+        auto cp1 = [&](int y) { r1[y] = old[U1 * PLANE + (y / TK) * PK + 2 + y % TK]; };
+        auto cp2 = [&](int y) { r2[y] = old[U2 * PLANE + 2 * PK + y]; };
         static_assert(PLANE <= 2 * NT && BU2_N <= 2 * NT && BU1_N <= 2 * NT, "two items at most");
-        copy(PLANE, [&](int x0) { bufs[x0] = old[U0 * PLANE + x0]; });
-        copy(BU2_N, [&](int y) { r1[y] = old[U1 * PLANE + (y / TK) * PK + 2 + y % TK]; });
-        copy(BU1_N, [&](int y) { r2[y] = old[U2 * PLANE + 2 * PK + y]; });
+        cp0(tid);
+        cp1(tid);
+        cp2(tid);
+        if constexpr (kStagger) {
+          // the conversion work is even across threads: deal the 368 extra
+          // items one per thread (u0 to 0..191, u1 to 192..319, u2 after)
+          if (tid < PLANE - NT) cp0(NT + tid);
+          else if (tid - (PLANE - NT) < BU2_N - NT) cp1(NT + tid - (PLANE - NT));
+          else if (tid - (PLANE - NT) - (BU2_N - NT) < BU1_N - NT)
+            cp2(NT + tid - (PLANE - NT) - (BU2_N - NT));
+        } else {
+          // extra items to the highest thread ids: the whole-plane arrival
+          // conversion gave its extra points to the lowest ones
+          auto extra = [&](int n, auto&& item) {
+            const int x = tid + n - 2 * NT;   // items NT..n-1 -> tids 2NT-n..NT-1
+            if (x >= 0 && n > NT) item(x + NT);
+          };
+          extra(PLANE, cp0);
+          extra(BU2_N, cp1);
+          extra(BU1_N, cp2);
+        }
       } else if constexpr (kGB) {
         // stored gradient boxes: TMA (issue_gb_tile)
       } else {
@@ -399,16 +482,20 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
 #pragma unroll
         for (int d = 0; d < 5; ++d) base[d] = sm + slot_of(d) * SLOT;
         if constexpr (TJ == 12) {
-        // items past the first NT of each buffer go to the threads that
-        // converted only one point of the new plane (tid >= PLANE - NT), so
-        // no warp carries much more than the average (max 9 vs 12 units,
-        // a conversion with its division ~3 units)
+        // items past the first NT of each buffer: D(u1,x1)'s and D(u2,x2)'s
+        // to threads 192..367; D(u0,x0)'s to threads 0..191 (staggered
+        // conversion) or also to 192..383 (whole-plane conversion, whose
+        // extra points sit on 0..191), so no warp carries much more than
+        // the average
         static_assert(PLANE - NT == 192 && BU1_N - NT == 48 && BU2_N - NT == 128,
                       "item split below assumes the 32 x 12 tile");
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
-          const int x0 = m == 0 ? tid : tid + 192;   // D(u0,x0), whole box
-          if (m == 0 || (tid >= 192 && x0 < PLANE)) {
+          // D(u0,x0), whole box; with the staggered conversion (even work
+          // per thread) its extra items go to threads 0..191, which take
+          // none of the other buffers' extras
+          const int x0 = m == 0 ? tid : (kStagger ? tid + 384 : tid + 192);
+          if (m == 0 || (kStagger ? tid < 192 : (tid >= 192 && x0 < PLANE))) {
             SAccW b;
 #pragma unroll
             for (int d = 0; d < 5; ++d) b.p[d] = base[d] + x0;
