@@ -155,12 +155,26 @@ def init_dist(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
-    if world > 1 and args.impl == "ours":
+    if (world > 1 or args.loopback) and args.impl == "ours":
         import torch
         import torch.distributed as dist
+        if world == 1:   # --loopback: a one-rank NCCL group of our own
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(free_port()))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
+
+
+def free_port() -> int:
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    return port
 
 
 def launcher_cmd(argv, gpus: int, port: int) -> list:
@@ -176,12 +190,7 @@ def self_launch(args, argv) -> int | None:
     torch.distributed.run with N ranks and return its exit code."""
     if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
         return None
-    import socket
-    sock = socket.socket()
-    sock.bind(("127.0.0.1", 0))
-    port = sock.getsockname()[1]
-    sock.close()
-    return subprocess.call(launcher_cmd(argv, args.gpus, port))
+    return subprocess.call(launcher_cmd(argv, args.gpus, free_port()))
 
 
 def cpu_cores() -> int:
@@ -281,7 +290,7 @@ def bench_variant(fd, variant, grid, cons_host, steps, warmup, flush_buf, lib,
     ev = fd.ResidualEvaluator(grid, c, variant)
     scheme = fd.RKScheme(dt=dt_of(grid.npoints))
     it = IterationState(state, saved=False)
-    multi = grid.slab is not None and grid.slab.nranks > 1
+    multi = grid.slab is not None and grid.slab.distributed
     for _ in range(warmup):
         _fused_iteration(it, scheme, ev)
     torch.cuda.synchronize()
@@ -525,7 +534,7 @@ def bench_e2e(fd, variant, grid, cons_host, steps):
         stepper.step()
     stepper.wait()
     torch.cuda.synchronize()
-    multi = grid.slab is not None and grid.slab.nranks > 1
+    multi = grid.slab is not None and grid.slab.distributed
     if multi:
         import torch.distributed as dist
         dist.barrier()
@@ -545,6 +554,7 @@ def bench_e2e(fd, variant, grid, cons_host, steps):
     npts = float(np.prod(grid.npoints))
     nbytes = host.numel() * 8
     wave = getattr(stepper, "wavefront", False)
+    graphs = getattr(stepper, "use_graphs", False)
     kw = getattr(stepper, "_wK", None)
     stepper.close() if hasattr(stepper, "close") else None
     del stepper, state, ev, host
@@ -563,7 +573,8 @@ def bench_e2e(fd, variant, grid, cons_host, steps):
                          "overlap)" if wave else
                          "; field copies in chunks, each upload chunk right "
                          "behind the previous result's download of it "
-                         f"({E2E_CHUNKS} chunks/field), CUDA graphs")
+                         f"({E2E_CHUNKS} chunks/field)"
+                         + (", CUDA graphs" if graphs else ""))
                      + ("; per rank: its slab" if multi else ""))}
 
 
@@ -651,15 +662,18 @@ def main_ours(args):
 
     n = args.n
     npts = global_grid(args, world)
-    slab = fd.Slab.from_process_group(npts[0]) if world > 1 else None
+    dist_on = world > 1 or args.loopback
+    slab = fd.Slab.from_process_group(npts[0], loopback=args.loopback) \
+        if dist_on else None
     grid = fd.make_grid(npts, (2 * np.pi,) * 3, slab=slab)
     npts_total = float(np.prod(grid.npoints))
     comm = None
-    if world > 1:
+    if dist_on:
         import torch.distributed as dist
         comm = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
                 "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
-                "local_planes": grid.local_npoints[0]}
+                "local_planes": grid.local_npoints[0],
+                "loopback": bool(args.loopback)}
     t0 = time.perf_counter()
     cons_host = taylor_green_conservative(grid, fd.PhysicalConstants())
     init_s = time.perf_counter() - t0
@@ -677,7 +691,7 @@ def main_ours(args):
             clocks, args.clock_window)
         v_mhz = median_mhz(clocks.rows[n_rows:])
         v_watts = median_watts(clocks.rows[n_rows:])
-        if world > 1:
+        if dist_on:
             import torch.distributed as dist
             t = torch.tensor([total_ms, cold_ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -713,7 +727,7 @@ def main_ours(args):
     e2e = bench_e2e(fd, head, grid, cons_host, max(3, min(args.steps,
                                                           args.e2e_steps)))
     if rank != 0:
-        if world > 1:
+        if dist_on:
             import torch.distributed as dist
             dist.barrier()
             dist.destroy_process_group()
@@ -759,7 +773,7 @@ def main_ours(args):
                              "variant's step right before its timed region"},
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
@@ -823,6 +837,10 @@ def parse_args(argv):
     ap.add_argument("--sizes", default="",
                     help="extra grid sizes for a single-stage sweep")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--loopback", action="store_true",
+                    help="one GPU as a one-rank z-slab over NCCL: the "
+                         "boundary/interior split and the axis-0 exchange "
+                         "(rank 0 -> rank 0) run as on N GPUs")
     args = ap.parse_args(argv)
     args.variants = [v.strip().upper() for v in args.variants.split(",")]
     if args.warmup < 3 and args.impl == "ours":

@@ -30,18 +30,27 @@ class Slab:
     offset0: int     # first global index owned
     local_n0: int
     group: object = None
+    loopback: bool = False   # one rank exchanging with itself over the backend
+
+    @property
+    def distributed(self) -> bool:
+        """Axis 0 goes through the exchange (several ranks, or a one-rank
+        loopback slab: the axis-0 ghosts then travel rank 0 -> rank 0 over
+        the communication backend, which runs the NCCL path on one GPU)."""
+        return self.nranks > 1 or self.loopback
 
     @staticmethod
-    def partition(n0: int, rank: int, nranks: int, group=None) -> "Slab":
+    def partition(n0: int, rank: int, nranks: int, group=None,
+                  loopback: bool = False) -> "Slab":
         base, rem = divmod(n0, nranks)
         local = base + (1 if rank < rem else 0)
         offset = rank * base + min(rank, rem)
-        return Slab(rank, nranks, n0, offset, local, group)
+        return Slab(rank, nranks, n0, offset, local, group, loopback)
 
     @staticmethod
-    def from_process_group(n0: int, group=None) -> "Slab":
+    def from_process_group(n0: int, group=None, loopback: bool = False) -> "Slab":
         return Slab.partition(n0, dist.get_rank(group), dist.get_world_size(group),
-                              group)
+                              group, loopback)
 
     def validate(self, n0: int, halo: int) -> None:
         from .mesh import ConfigurationError

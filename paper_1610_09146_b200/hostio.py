@@ -167,7 +167,7 @@ class HostStepper:
             raise ValueError("upload must be 'sm' or 'ce'")
         self.upload = upload
         slab = state.grid.slab
-        single = slab is None or slab.nranks == 1
+        single = slab is None or not slab.distributed
         self.use_graphs = single if graphs is None else graphs
         self._graphs = None
         self._pending = False   # the last step's result is not downloaded yet

@@ -194,7 +194,7 @@ def halo_exchange_bundle(grid: Grid, bundle: torch.Tensor, nf: int | None = None
     lib = _lib.load()
     nf = bundle.shape[0] if nf is None else nf
     pb = grid.problem()
-    multi = grid.slab is not None and grid.slab.nranks > 1
+    multi = grid.slab is not None and grid.slab.distributed
     mask = 0b110 if multi else 0b111
     _lib.check(lib.fdns_halo_wrap(_lib.ptr(bundle), nf, mask, pb,
                                   _lib.stream_handle()), "halo wrap")
@@ -212,6 +212,6 @@ def halo_exchange(field: Field) -> Field:
 def reduce_sum(field: Field) -> float:
     """Sum over interior points (mesh.py:142-148), across slab ranks."""
     s = field.interior.sum()
-    if field.grid.slab is not None and field.grid.slab.nranks > 1:
+    if field.grid.slab is not None and field.grid.slab.distributed:
         s = field.grid.slab.allreduce_sum(s.reshape(1))[0]
     return float(s)

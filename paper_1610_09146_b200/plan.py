@@ -392,7 +392,7 @@ class ResidualEvaluator:
         """Axes whose ghosts the stage kernel fills in place (all three on
         one GPU; axis 0 comes from the slab exchange on several)."""
         slab = self.grid.slab
-        return 0b110 if slab is not None and slab.nranks > 1 else 0b111
+        return 0b110 if slab is not None and slab.distributed else 0b111
 
     def stage(self, inp: torch.Tensor, saved: torch.Tensor, out: torch.Tensor,
               coef: float) -> None:
