@@ -253,11 +253,13 @@ struct InlineProvider {
   const Coef& k;
   const Acc& a;
   __device__ InlineProvider(const Coef& k_, const Acc& a_) : k(k_), a(a_) {}
-  template <int A_, int L, int OCC = 0> __device__ __forceinline__ double g() const {
-    return eval_slot<A_, L>(k, occurrence_view<OCC>(a));
+  template <int A_, int L, int OCC = 0, bool DES = false> __device__ __forceinline__ double g() const {
+    if constexpr (DES && Acc::kMaskTaps) return eval_slot<A_, L>(k, a);   // designated
+    else return eval_slot<A_, L>(k, occurrence_view<OCC>(a));
   }
-  template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const {
-    return dd<O, J>(k, occurrence_view<OCC>(a));
+  template <int J, int O, int OCC = 0, bool DES = false> __device__ __forceinline__ double x() const {
+    if constexpr (DES && Acc::kMaskTaps) return dd<O, J>(k, a);
+    else return dd<O, J>(k, occurrence_view<OCC>(a));
   }
 };
 
@@ -280,18 +282,18 @@ struct LocalProvider {
     v[S_DD + dd_index(0, 2)] = dd<2, 0>(k, a);
     v[S_DD + dd_index(1, 2)] = dd<2, 1>(k, a);
   }
-  template <int A_, int L, int OCC = 0> __device__ __forceinline__ double g() const { return v[slot(A_, L)]; }
-  template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const { return v[S_DD + dd_index(J, O)]; }
+  template <int A_, int L, int OCC = 0, bool DES = false> __device__ __forceinline__ double g() const { return v[slot(A_, L)]; }
+  template <int J, int O, int OCC = 0, bool DES = false> __device__ __forceinline__ double x() const { return v[S_DD + dd_index(J, O)]; }
 };
 
 // FETCH (BL): every derivative read from its work array at the point.
 struct FetchProvider {
   const double* __restrict__ wa;
   int64_t c, fs;
-  template <int A_, int L, int OCC = 0> __device__ __forceinline__ double g() const {
+  template <int A_, int L, int OCC = 0, bool DES = false> __device__ __forceinline__ double g() const {
     return __ldg(wa + slot(A_, L) * fs + c);
   }
-  template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const {
+  template <int J, int O, int OCC = 0, bool DES = false> __device__ __forceinline__ double x() const {
     return __ldg(wa + (S_DD + dd_index(J, O)) * fs + c);
   }
 };
@@ -309,12 +311,12 @@ struct SSProvider {
   __device__ SSProvider(const Coef& k_, const Acc& a_, const double* ws_, int64_t c_, int64_t fs_,
                         int64_t s0, int64_t s1)
       : k(k_), a(a_), ws(ws_), c(c_), fs(fs_) { st[0] = s0; st[1] = s1; st[2] = 1; }
-  template <int A_, int L, int OCC = 0> __device__ __forceinline__ double g() const {
+  template <int A_, int L, int OCC = 0, bool DES = false> __device__ __forceinline__ double g() const {
     if constexpr (L >= S_U && L < S_U + 3) return __ldg(ws + ((L - S_U) * 3 + A_) * fs + c);
     else if constexpr (INLINE_REST) return eval_slot<A_, L>(k, occurrence_view<OCC>(a));
     else return eval_slot<A_, L>(k, a);
   }
-  template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const {
+  template <int J, int O, int OCC = 0, bool DES = false> __device__ __forceinline__ double x() const {
     return d1_stored(k, O, ws + (J * 3 + J) * fs, c, st[O]);
   }
 };
@@ -347,12 +349,43 @@ struct SSProvider {
 #ifndef FDNS_RA_PER_EQUATION
 #define FDNS_RA_PER_EQUATION 0
 #endif
+//
+// Designated occurrences (round 2): an opaque mask is only needed to keep
+// an occurrence apart from the *other* occurrences of the same derivative,
+// so each of the 60 derivatives has exactly one call site evaluated from
+// the plain accessor (GD / XD with the designation condition and group)
+// and every other one masked.  All 117 occurrences are still evaluated
+// separately -- every first-level operation of a masked occurrence has a
+// masked operand, so none can merge with the designated one; the static
+// FP64 count of the RA stage kernel is unchanged (1324) -- but only 57 of
+// them are masked.  Groups (bits of FDNS_RA_DESIGNATED, default 27 = 0, 1,
+// 3, 4): 0 the only occurrence of its derivative (D(rho), D(p), the
+// convective products, D(rhoE), D(rhoE u), D(u p), D2(T), D(rhou_i, x_a)
+// for a != i); 1 mass's D(rhou_a, x_a) and D(u_a, x_a); 3 the energy's
+// off-diagonal D(u_i, x_j) stress-work multipliers; 4 the energy's viscous
+// D2 and mixed terms (group 2 designates momentum's instead: 2.2 KB of
+// spills in the 12-warp kernel).  12-warp RA kernel: 6248 -> 5912 static
+// instructions, whole RK3 steps +6.4% (256^3) / +5.8% (512^3), RS
+// unaffected (its providers ignore the designation;
+// profiles/r02_ra_designated_ab.txt).
+#ifndef FDNS_RA_DESIGNATED
+#define FDNS_RA_DESIGNATED 27   // bit mask of the designated groups below
+#endif
 #if FDNS_RA_PER_EQUATION
 #define G(a, L) P.template g<a, L, EQ>()
 #define X(j, o) P.template x<j, o, EQ>()
+#define GD(grp, c, a, L) G(a, L)
+#define XD(grp, j, o) X(j, o)
 #else
 #define G(a, L) P.template g<a, L, SALT * 64 + __COUNTER__>()
 #define X(j, o) P.template x<j, o, SALT * 64 + __COUNTER__>()
+// designated when `c` holds and group `grp` is enabled: 0 = the only
+// occurrence of its derivative; 1 = mass; 2 = momentum's viscous terms;
+// 3 = the energy's stress-work multipliers
+#define GD(grp, c, a, L) \
+  P.template g<a, L, SALT * 64 + __COUNTER__, bool((c) && ((FDNS_RA_DESIGNATED >> (grp)) & 1))>()
+#define XD(grp, j, o) \
+  P.template x<j, o, SALT * 64 + __COUNTER__, bool((FDNS_RA_DESIGNATED >> (grp)) & 1)>()
 #endif
 
 template <int I, class Pv>
@@ -362,8 +395,8 @@ __device__ __forceinline__ double viscous(const Coef& k, const Pv& P) {
   // (terms.py:113-123)
   constexpr int J1 = I == 0 ? 1 : 0;
   constexpr int J2 = I == 2 ? 1 : 2;
-  return k.c43 * G(I, S_U2 + I) + k.inv_Re * G(J1, S_U2 + I) + k.c13 * X(J1, I) +
-         k.inv_Re * G(J2, S_U2 + I) + k.c13 * X(J2, I);
+  return k.c43 * GD(4, true, I, S_U2 + I) + k.inv_Re * GD(4, true, J1, S_U2 + I) +
+         k.c13 * XD(4, J1, I) + k.inv_Re * GD(4, true, J2, S_U2 + I) + k.c13 * XD(4, J2, I);
 }
 
 // Momentum i, split into the chain prefix -(0.5*(conv)) - D(p,x_i) and the
@@ -374,10 +407,10 @@ template <int I, class Pv>
 __device__ __forceinline__ double momentum_prefix(const Coef& k, const Pv& P, const double* r) {
   [[maybe_unused]] constexpr int SALT = 4 + I, EQ = 1 + I;
   const double rui = r[RU0 + I];
-  const double conv = G(0, S_RUU + I) + r[U0] * G(0, S_RU + I) + rui * G(0, S_U + 0) +
-                      G(1, S_RUU + I) + r[U1] * G(1, S_RU + I) + rui * G(1, S_U + 1) +
-                      G(2, S_RUU + I) + r[U2] * G(2, S_RU + I) + rui * G(2, S_U + 2);
-  return -(0.5 * conv) - G(I, S_P);
+  const double conv = GD(0, true, 0, S_RUU + I) + r[U0] * GD(0, I != 0, 0, S_RU + I) + rui * G(0, S_U + 0) +
+                      GD(0, true, 1, S_RUU + I) + r[U1] * GD(0, I != 1, 1, S_RU + I) + rui * G(1, S_U + 1) +
+                      GD(0, true, 2, S_RUU + I) + r[U2] * GD(0, I != 2, 2, S_RU + I) + rui * G(2, S_U + 2);
+  return -(0.5 * conv) - GD(0, true, I, S_P);
 }
 
 template <int I, class Pv>
@@ -385,8 +418,8 @@ __device__ __forceinline__ double momentum_suffix(const Coef& k, const Pv& P, do
   [[maybe_unused]] constexpr int SALT = 10 + I, EQ = 1 + I;
   constexpr int J1 = I == 0 ? 1 : 0;
   constexpr int J2 = I == 2 ? 1 : 2;
-  return pre + k.c43 * G(I, S_U2 + I) + k.inv_Re * G(J1, S_U2 + I) + k.c13 * X(J1, I) +
-         k.inv_Re * G(J2, S_U2 + I) + k.c13 * X(J2, I);
+  return pre + k.c43 * GD(2, true, I, S_U2 + I) + k.inv_Re * GD(2, true, J1, S_U2 + I) + k.c13 * XD(2, J1, I) +
+         k.inv_Re * GD(2, true, J2, S_U2 + I) + k.c13 * XD(2, J2, I);
 }
 
 template <int I, class Pv>
@@ -408,9 +441,9 @@ __device__ __forceinline__ double tau(const Coef& k, const Pv& P) {
 template <class Pv>
 __device__ __forceinline__ double mass_residual(const Coef& k, const Pv& P, const double* r) {
   [[maybe_unused]] constexpr int SALT = 13, EQ = 0;
-  const double acc = G(0, S_RU + 0) + r[U0] * G(0, S_RHO) + r[RHO] * G(0, S_U + 0) +
-                     G(1, S_RU + 1) + r[U1] * G(1, S_RHO) + r[RHO] * G(1, S_U + 1) +
-                     G(2, S_RU + 2) + r[U2] * G(2, S_RHO) + r[RHO] * G(2, S_U + 2);
+  const double acc = GD(1, true, 0, S_RU + 0) + r[U0] * GD(0, true, 0, S_RHO) + r[RHO] * GD(1, true, 0, S_U + 0) +
+                     GD(1, true, 1, S_RU + 1) + r[U1] * GD(0, true, 1, S_RHO) + r[RHO] * GD(1, true, 1, S_U + 1) +
+                     GD(1, true, 2, S_RU + 2) + r[U2] * GD(0, true, 2, S_RHO) + r[RHO] * GD(1, true, 2, S_U + 2);
   return -(0.5 * acc);
 }
 
@@ -421,16 +454,16 @@ __device__ __forceinline__ double energy_prefix(const Coef& k, const Pv& P, cons
   const double rhoe = RHOE_INTERNAL ? r[RHOE_F]
                                     : r[RHOE_F] - 0.5 * (r[RU0] * r[U0] + r[RU1] * r[U1] +
                                                          r[RU2] * r[U2]);
-  const double conv = G(0, S_RHOEU) + r[U0] * G(0, S_RHOE) + rhoe * G(0, S_U + 0) +
-                      G(1, S_RHOEU) + r[U1] * G(1, S_RHOE) + rhoe * G(1, S_U + 1) +
-                      G(2, S_RHOEU) + r[U2] * G(2, S_RHOE) + rhoe * G(2, S_U + 2);
-  const double pwork = G(0, S_UP) + G(1, S_UP) + G(2, S_UP);
-  const double heat = k.heat * (G(0, S_T2) + G(1, S_T2) + G(2, S_T2));
+  const double conv = GD(0, true, 0, S_RHOEU) + r[U0] * GD(0, true, 0, S_RHOE) + rhoe * G(0, S_U + 0) +
+                      GD(0, true, 1, S_RHOEU) + r[U1] * GD(0, true, 1, S_RHOE) + rhoe * G(1, S_U + 1) +
+                      GD(0, true, 2, S_RHOEU) + r[U2] * GD(0, true, 2, S_RHOE) + rhoe * G(2, S_U + 2);
+  const double pwork = GD(0, true, 0, S_UP) + GD(0, true, 1, S_UP) + GD(0, true, 2, S_UP);
+  const double heat = k.heat * (GD(0, true, 0, S_T2) + GD(0, true, 1, S_T2) + GD(0, true, 2, S_T2));
   return -(0.5 * conv) - (pwork) + heat +
-         tau<0, 0>(k, P) * G(0, S_U + 0) + tau<0, 1>(k, P) * G(1, S_U + 0) +
-         tau<0, 2>(k, P) * G(2, S_U + 0) + tau<1, 0>(k, P) * G(0, S_U + 1) +
-         tau<1, 1>(k, P) * G(1, S_U + 1) + tau<1, 2>(k, P) * G(2, S_U + 1) +
-         tau<2, 0>(k, P) * G(0, S_U + 2) + tau<2, 1>(k, P) * G(1, S_U + 2) +
+         tau<0, 0>(k, P) * G(0, S_U + 0) + tau<0, 1>(k, P) * GD(3, true, 1, S_U + 0) +
+         tau<0, 2>(k, P) * GD(3, true, 2, S_U + 0) + tau<1, 0>(k, P) * GD(3, true, 0, S_U + 1) +
+         tau<1, 1>(k, P) * G(1, S_U + 1) + tau<1, 2>(k, P) * GD(3, true, 2, S_U + 1) +
+         tau<2, 0>(k, P) * GD(3, true, 0, S_U + 2) + tau<2, 1>(k, P) * GD(3, true, 1, S_U + 2) +
          tau<2, 2>(k, P) * G(2, S_U + 2);
 }
 
@@ -464,6 +497,8 @@ __device__ __forceinline__ void residual_point(const Coef& k, const Pv& P, const
 }
 #undef G
 #undef X
+#undef GD
+#undef XD
 
 // Fused primitive recovery of one point (physics.py:185-202).
 __device__ __forceinline__ void primitives_point(const Coef& k, const double* q, double* prim) {

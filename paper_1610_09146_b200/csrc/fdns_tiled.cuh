@@ -293,8 +293,8 @@ struct TiledLocalProvider {
     v[S_DD + dd_index(2, 1)] = k.w1[1] * (bu2[PK] - bu2[-PK]) + k.w2[1] * (bu2[2 * PK] - bu2[-2 * PK]);
     v[S_DD + dd_index(1, 2)] = k.w1[2] * (bu1[1] - bu1[-1]) + k.w2[2] * (bu1[2] - bu1[-2]);
   }
-  template <int A_, int L, int OCC = 0> __device__ __forceinline__ double g() const { return v[slot(A_, L)]; }
-  template <int J, int O, int OCC = 0> __device__ __forceinline__ double x() const { return v[S_DD + dd_index(J, O)]; }
+  template <int A_, int L, int OCC = 0, bool DES = false> __device__ __forceinline__ double g() const { return v[slot(A_, L)]; }
+  template <int J, int O, int OCC = 0, bool DES = false> __device__ __forceinline__ double x() const { return v[S_DD + dd_index(J, O)]; }
 };
 
 // Lazily evaluated SN provider over the staged tile: a derivative is
@@ -309,7 +309,7 @@ struct TiledLazyProviderT {
   const double* b0;   // D(u0,x0) centre of the box buffer (pitch PK)
   const double* b1;   // D(u1,x1) centre (pitch PK)
   const double* b2;   // D(u2,x2) centre (pitch B2P)
-  template <int A_, int L, int OCC = 0>
+  template <int A_, int L, int OCC = 0, bool DES = false>
   __device__ __forceinline__ double g() const {
     if constexpr (L == S_U + A_) {
       if constexpr (A_ == 0) return b0[0];
@@ -319,7 +319,7 @@ struct TiledLazyProviderT {
       return eval_slot<A_, L>(k, a);
     }
   }
-  template <int J, int O, int OCC = 0>
+  template <int J, int O, int OCC = 0, bool DES = false>
   __device__ __forceinline__ double x() const {
     if constexpr (O == 0) {
       const double* q = J == 1 ? q1 : q2;
@@ -353,7 +353,7 @@ struct TiledSSProviderT {
   const double* gb1;  // stored D(u1,x1)
   const double* gb2;  // stored D(u2,x2) (row pitch B2P)
   const double* gv;   // off-diagonal D(u_q,x_a) at the point, [q*3+a]
-  template <int A_, int L, int OCC = 0>
+  template <int A_, int L, int OCC = 0, bool DES = false>
   __device__ __forceinline__ double g() const {
     if constexpr (L >= S_U && L < S_U + 3) {
       constexpr int q = L - S_U;
@@ -365,7 +365,7 @@ struct TiledSSProviderT {
       return eval_slot<A_, L>(k, a);
     }
   }
-  template <int J, int O, int OCC = 0>
+  template <int J, int O, int OCC = 0, bool DES = false>
   __device__ __forceinline__ double x() const {
     if constexpr (O == 0) {
       const double* q = J == 1 ? q1 : q2;
