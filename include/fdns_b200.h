@@ -141,10 +141,17 @@ void fdns_set_pdl(int32_t enabled);
  * stored gradients.  A kill switch and an A/B hook. */
 void fdns_set_prefetch(int32_t mask);
 
-/* Test hook: unit size (planes) of the SS/RS round-robin split (-1 =
- * default: 64-plane units from 256 planes; 0 = off; c > 0 = c-plane units
- * wherever the plane count is a multiple of c and at least 4c). */
+/* Test hook: unit size (planes) of the round-robin split of the SS, RS and
+ * SN stage kernels (-1 = default: SS/RS 64-plane units from 256 planes, SS/RS
+ * and SN 128-plane units from 512; 0 = off; c > 0 = c-plane units wherever
+ * the plane count is a multiple of c and at least 2c). */
 void fdns_set_rounds(int32_t planes);
+
+/* Lockstep of the round-robin CTAs: a CTA waits while a tile-grid neighbour
+ * is more than `slack` step barriers behind, so the halos they share hit in
+ * L2 (-1 = default, 2; 0 = free running).  A kill switch and an A/B hook;
+ * results do not depend on it. */
+void fdns_set_lockstep(int32_t slack);
 
 /* Debug timeline of the tiled stage kernels: enable (1) / disable (0) the
  * per-CTA %globaltimer stamps (entry, prologue done, first window ready,

@@ -59,6 +59,7 @@ EXPORTS = {
     "fdns_set_pdl": (None, [_I]),
     "fdns_set_prefetch": (None, [_I]),
     "fdns_set_rounds": (None, [_I]),
+    "fdns_set_lockstep": (None, [_I]),
     "fdns_debug_trace": (_I, [_I, ctypes.POINTER(ctypes.c_uint64), _I]),
     "fdns_diag_partials_size": (_I, [ctypes.POINTER(Problem)]),
     "fdns_reduce_diag": (_I, [_VP, _VP, _VP, _VP, ctypes.POINTER(Problem),

@@ -574,6 +574,69 @@ __global__ void __launch_bounds__(256) k_grad_ss_interior(const double* __restri
   ws[(2 * 3 + 2) * g.fs + c] = d1<2, E_FIELD, U2, 0>(k, a);
 }
 
+// The same fill, two axis-2 neighbours per thread through 16-byte accesses:
+// a thread owns the padded columns (2t, 2t+1) of a 64-column block, so its
+// pair is 16-byte aligned (even halo, even row pitch) and lies wholly inside
+// or outside the interior.  Per velocity field the axis-2 taps of both points
+// are three vector loads, the axis-1 and axis-0 taps four each: 33 loads + 9
+// stores per pair instead of 72 + 18 -- the one-point kernel is bound by its
+// load/store instruction queue (ncu: lg throttle 8.9, long scoreboard 27
+// cycles per issue).  Same expressions per point (d1: stencil.py:80-84), so
+// the bits are unchanged.
+// Blocks past the interior planes (blockIdx.z >= n0) compute the diagonal
+// arrays' ghost frames (k_diag_ghost semantics, f0 + f1 + f2 points; they
+// read only the state): dispatched last, they fill the launch's tail
+// instead of a separate, latency-bound 87 us kernel.
+__global__ void __launch_bounds__(256) k_grad_ss_pair(const double* __restrict__ in,
+                                                      double* __restrict__ ws, Coef k, Geom g,
+                                                      int64_t f0, int64_t f1, int64_t f2) {
+  pdl_entry();
+  if ((int)blockIdx.z >= g.n0) {
+    const int64_t blk = ((int64_t)(blockIdx.z - g.n0) * gridDim.y + blockIdx.y) * gridDim.x +
+                        blockIdx.x;
+    const int64_t t = blk * 256 + threadIdx.y * 32 + threadIdx.x;
+    if (t < f0) diag_ghost_point<0>(in, ws + 0 * g.fs, k, g, t);
+    else if (t < f0 + f1) diag_ghost_point<1>(in, ws + 4 * g.fs, k, g, t - f0);
+    else if (t < f0 + f1 + f2) diag_ghost_point<2>(in, ws + 8 * g.fs, k, g, t - f0 - f1);
+    return;
+  }
+  const int pk = (int)(blockIdx.x * 64 + 2 * threadIdx.x);   // padded column of the pair
+  const int kk = pk - g.h;
+  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
+  const int ii = blockIdx.z;
+  if (kk < 0 || kk >= g.n2 || jj >= g.n1) return;
+  const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + pk;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const double* u = in + (U0 + q) * g.fs + c;
+    auto ld2 = [&](int64_t off) { return __ldg(reinterpret_cast<const double2*>(u + off)); };
+    // axis 0 and axis 1: the pair's taps sit in the same 16 bytes
+    double2 d[2];
+#pragma unroll
+    for (int ax = 0; ax < 2; ++ax) {
+      const int64_t st = ax == 0 ? g.s0 : g.s1;
+      const double2 p1 = ld2(st), m1 = ld2(-st), p2 = ld2(2 * st), m2 = ld2(-2 * st);
+      d[ax].x = k.w1[ax] * (p1.x - m1.x) + k.w2[ax] * (p2.x - m2.x);
+      d[ax].y = k.w1[ax] * (p1.y - m1.y) + k.w2[ax] * (p2.y - m2.y);
+    }
+    // axis 2: columns pk-2 .. pk+3
+    const double2 a = ld2(-2), b = ld2(0), e = ld2(2);
+    double2 d2v;
+    d2v.x = k.w1[2] * (b.y - a.y) + k.w2[2] * (e.x - a.x);
+    d2v.y = k.w1[2] * (e.x - b.x) + k.w2[2] * (e.y - a.y);
+    double* w = ws + (q * 3) * g.fs + c;
+    *reinterpret_cast<double2*>(w) = d[0];
+    *reinterpret_cast<double2*>(w + g.fs) = d[1];
+    *reinterpret_cast<double2*>(w + 2 * g.fs) = d2v;
+  }
+}
+// whether k_grad_ss_pair applies: 16-byte aligned pairs that never straddle
+// the interior's edge
+inline bool ss_pair_ok(const Geom& g, const double* in, const double* ws) {
+  return g.h == 2 && (g.n2 & 1) == 0 && (g.s1 & 1) == 0 && (g.s0 & 1) == 0 && (g.fs & 1) == 0 &&
+         ((uintptr_t)in & 15) == 0 && ((uintptr_t)ws & 15) == 0;
+}
+
 // RK update on the interior of 5 fields (timeloop.py:80-85).
 __global__ void k_rk_update(double* cons, const double* saved, const double* __restrict__ res,
                             double coef, Geom g) {
@@ -982,26 +1045,43 @@ std::vector<int64_t> table_cuts(int64_t G, const TileCost& tc, int planes) {
 
 struct Launch { int64_t ctas; int aligned; const int64_t* cuts; };
 
-// Round-robin units (tiled::SPLIT_ROUNDS) for the SS/RS stage kernel: units
-// of ROUND_PLANES planes of one tile, dealt chunk-major, so neighbouring
-// tiles are staged at the same time and their shared halo columns (state
-// and the stored gradient boxes) hit in L2.  Measured whole RK3 steps at
-// 256^3: SS +6.4%, RS +1.8% with 64-plane units (32: +4.8% / 0%; 16:
-// slower); at 128^3 the extra ramps cost more than the L2 hits win (SS
-// -1.7%), and SN/RA (FP64-bound, far from the HBM roof) lose 5-9% at every
-// size, so only SS/RS from 256 planes use it.  FDNS_ROUNDS=C overrides the
-// unit (0 disables).
-// Round 2, 12-warp kernel: SN with 64/128-plane units cut its DRAM reads
-// (31.4 -> ~25 GB per stage at 512^3) but its step time moved by -0.1% to
-// +3% depending on the box (profiles/r02_rr_sn_ra_ab.txt), RA by -0.4%:
-// both keep the contiguous split.
-constexpr int ROUND_PLANES = 64;
+// Round-robin units (tiled::SPLIT_ROUNDS): units of c planes of one tile,
+// dealt chunk-major, so neighbouring tiles are staged at the same time and
+// their shared halo columns and rows (state boxes, stored gradient boxes)
+// can hit in L2.  Round 1 (SS/RS, 64-plane units): whole RK3 steps at 256^3
+// SS +6.4%, RS +1.8%; at 128^3 the extra ramps cost more than the L2 hits
+// win, so it is on from 256 planes.
+// Round 2: free-running CTAs drift apart, so most of those halos still came
+// from DRAM (ncu at 512^3: SS stage kernel 36.5 GB of reads for 23.6 GB of
+// inputs).  With the CTAs held in lockstep (fdns_tiled.cuh:ls_step, K = 2
+// steps of slack) the reads are 26.5 GB (1.12x) and SN's 15.2 GB (1.08x,
+// 25.5 GB with the contiguous split); with the last, partial round cut into
+// equal plane ranges (Segments::partition) no SM idles through it.  Whole
+// RK3 steps at 512^3, interleaved A/B (profiles/r02_lockstep_ab.txt):
+// SS +6%, RS +7%, SN +2-3% (128-plane units); RA -3% (FP64-bound and the
+// least power-capped variant: it keeps the contiguous split).
+// FDNS_ROUNDS=c overrides the unit (0 = off), FDNS_ROUNDS_ALL=1 adds RA,
+// FDNS_LOCKSTEP=K sets the slack (0 = free running).
 int g_rounds_env = std::getenv("FDNS_ROUNDS") ? std::atoi(std::getenv("FDNS_ROUNDS")) : -1;
+int g_rounds_all = std::getenv("FDNS_ROUNDS_ALL") ? std::atoi(std::getenv("FDNS_ROUNDS_ALL")) : 0;
+int g_lockstep = std::getenv("FDNS_LOCKSTEP") ? std::atoi(std::getenv("FDNS_LOCKSTEP")) : 2;
 inline int rounds_planes(int variant, int nplanes) {
-  if (variant != FDNS_SS && variant != FDNS_RS) return 0;
-  const int c = g_rounds_env >= 0 ? g_rounds_env : ROUND_PLANES;
-  if (c <= 0 || nplanes % c != 0 || nplanes < 4 * c || g_tiled_ctas > 0) return 0;
-  return c;
+  const bool gb = variant == FDNS_SS || variant == FDNS_RS;
+  if (!gb && variant != FDNS_SN && !(variant == FDNS_RA && g_rounds_all)) return 0;
+  if (g_rounds_env >= 0) {
+    const int c = g_rounds_env;
+    return (c <= 0 || nplanes % c != 0 || nplanes < 2 * c) ? 0 : c;
+  }
+  // defaults: SS/RS from 256 planes, SN from 512; 128-plane units where
+  // they divide the planes, else 64
+  if (nplanes < (gb ? 256 : 512)) return 0;
+  if (nplanes % 128 == 0) return 128;
+  return nplanes % 64 == 0 ? 64 : 0;
+}
+// CTAs of a round-robin launch over `units` units
+inline unsigned rounds_ctas(int64_t units) {
+  const int64_t cap = g_tiled_ctas > 0 ? g_tiled_ctas : num_sms();
+  return (unsigned)std::min<int64_t>(cap, units);
 }
 
 Launch pick_launch(int ntk, int ntj, int planes, int wrap, int variant, cudaStream_t s,
@@ -1095,14 +1175,15 @@ int launch_tiled_v(const CUtensorMap& m, const double* in, const double* saved, 
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
   if constexpr (V == FDNS_SS || V == FDNS_RS) {
-    if (const int c = rounds_planes(V, nplanes)) {
+    if (const int c = total < (1ll << 31) ? rounds_planes(V, nplanes) : 0) {
+      pf |= (g_lockstep & 0xff) << 8;
       static std::atomic<uint64_t> attr_rr{0};
       once_per_device(attr_rr, [] {
         cudaFuncSetAttribute(tiled::k_stage_tiled<V, MODE, LAZY, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       });
       launch_pdl(tiled::k_stage_tiled<V, MODE, LAZY, true>,
-                 dim3((unsigned)std::min<int64_t>(num_sms(), total / c)), dim3(tiled::NT), smem,
+                 dim3(rounds_ctas(total / c)), dim3(tiled::NT), smem,
                  s, m, mg, ms, mp, work, saved, out, k, g, coef, ntk, total, wrap, i_lo, c,
                  (int)tiled::SPLIT_ROUNDS, pf, (const int64_t*)nullptr);
       return 0;
@@ -1169,15 +1250,16 @@ int launch_t12(const double* in, const double* saved, double* out, const double*
   const int ntj = (g.n1 + L::TJ - 1) / L::TJ;
   const int nplanes = i_hi - i_lo;
   const int64_t total = (int64_t)ntk * ntj * nplanes;
-  if constexpr (gb) {
-    if (const int c = rounds_planes(V, nplanes)) {   // round-robin units (SS/RS)
+  {
+    if (const int c = total < (1ll << 31) ? rounds_planes(V, nplanes) : 0) {   // round-robin units (SS/RS)
+      pf |= (g_lockstep & 0xff) << 8;
       static std::atomic<uint64_t> attr_rr{0};
       once_per_device(attr_rr, [] {
         cudaFuncSetAttribute(t12::k_stage_t12<V, MODE, TJ_, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_BYTES);
       });
       launch_pdl(t12::k_stage_t12<V, MODE, TJ_, true>,
-                 dim3((unsigned)std::min<int64_t>(num_sms(), total / c)), dim3(L::NT),
+                 dim3(rounds_ctas(total / c)), dim3(L::NT),
                  L::SMEM_BYTES, s, m, ms, gm, work, saved, out, k, g, coef, ntk, total, wrap,
                  i_lo, c, (int)tiled::SPLIT_ROUNDS, pf, (const int64_t*)nullptr);
       return 0;
@@ -1264,6 +1346,9 @@ inline int march_fill_mode(const Geom& g) {
 }
 // A/B switch: FDNS_SS_FILL_1D=1 selects the one-launch grid-stride SS fill.
 const bool g_ss_fill_3d = std::getenv("FDNS_SS_FILL_1D") == nullptr;
+// FDNS_SS_FILL_PAIR=0: the one-point-per-thread interior fill (A/B)
+const bool g_ss_fill_pair =
+    !(std::getenv("FDNS_SS_FILL_PAIR") && std::atoi(std::getenv("FDNS_SS_FILL_PAIR")) == 0);
 
 // Work-array fills that precede the residual kernel (BL, RS, SS).
 int launch_fills(int variant, const double* in, double* work, const Coef& k, const Geom& g,
@@ -1319,9 +1404,22 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
   // frames (+6% SS/RS steps at 256^3); below, one grid-stride launch
   // (its single launch wins at 64^3: -4% otherwise)
   if ((variant == FDNS_SS || variant == FDNS_RS) && g_ss_fill_3d && g.n2 >= 128) {
-    k_grad_ss_interior<<<grd, blk, 0, s>>>(in, work, k, g);
-    ghosts(work + 0 * g.fs, work + 4 * g.fs, work + 8 * g.fs, false);
-    count(2);
+    if (g_ss_fill_pair && ss_pair_ok(g, in, work)) {
+      // interior planes + the z layers of blocks that cover the ghost frames
+      const int h = g.h;
+      const int64_t f0 = (int64_t)g.n0 * (2 * h * (g.n2 + 2 * h) + (int64_t)g.n1 * 2 * h);
+      const int64_t f1 = (int64_t)g.n1 * (2 * h * (g.n2 + 2 * h) + (int64_t)g.n0 * 2 * h);
+      const int64_t f2 = (int64_t)g.n2 * (2 * h * (g.n1 + 2 * h) + (int64_t)g.n0 * 2 * h);
+      dim3 pgrd((unsigned)((g.n2 + 2 * g.h + 63) / 64), grd.y, grd.z);
+      const int64_t per_layer = (int64_t)256 * pgrd.x * pgrd.y;
+      pgrd.z += (unsigned)((f0 + f1 + f2 + per_layer - 1) / per_layer);
+      k_grad_ss_pair<<<pgrd, blk, 0, s>>>(in, work, k, g, f0, f1, f2);
+      count(1);
+    } else {
+      k_grad_ss_interior<<<grd, blk, 0, s>>>(in, work, k, g);
+      ghosts(work + 0 * g.fs, work + 4 * g.fs, work + 8 * g.fs, false);
+      count(2);
+    }
     return check_launch("SS fills");
   }
   if (variant == FDNS_SS || variant == FDNS_RS) {
@@ -1360,6 +1458,8 @@ void fdns_set_tiled_grid(int32_t ctas) { g_tiled_ctas = ctas; }
 void fdns_set_pdl(int32_t enabled) { g_pdl = enabled != 0; }
 
 void fdns_set_rounds(int32_t planes) { g_rounds_env = planes; }
+
+void fdns_set_lockstep(int32_t slack) { g_lockstep = slack < 0 ? 2 : std::min(slack, 255); }
 
 void fdns_set_prefetch(int32_t mask) {
   g_prefetch_saved = (mask & 1) != 0;

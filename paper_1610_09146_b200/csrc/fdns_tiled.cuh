@@ -104,6 +104,43 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (clock64() - t0 > 4000000000LL) __trap();
   }
 }
+#ifndef FDNS_ST_CS
+#define FDNS_ST_CS 0
+#endif
+#ifndef FDNS_LD_CS
+#define FDNS_LD_CS 0
+#endif
+#ifndef FDNS_TMA_EL
+#define FDNS_TMA_EL 0
+#endif
+// streaming (evict-first) load of a value read once per stage
+__device__ __forceinline__ double ld_stream(const double* p) {
+#if FDNS_LD_CS
+  return __ldcs(p);
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ double ldg_stream(const double* p) {
+#if FDNS_LD_CS
+  return __ldcs(p);
+#else
+  return __ldg(p);
+#endif
+}
+// state boxes with an L2 evict-last hint (their halo columns are re-read by
+// the neighbouring tiles' CTAs)
+__device__ __forceinline__ void tma_load_plane_el(double* dst, const CUtensorMap* map,
+                                                  uint64_t* bar, int c0, int c1, int c2) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(0), "r"(saddr(bar)),
+      "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_plane(double* dst, const CUtensorMap* map, uint64_t* bar,
                                                int c0, int c1, int c2) {
   asm volatile(
@@ -176,7 +213,13 @@ __device__ __forceinline__ void emit_general(double* out, const Geom& g, int i, 
 template <int NOUT>
 __device__ __forceinline__ void emit_at(double* out, const Geom& g, int64_t c, const double* val) {
 #pragma unroll
-  for (int f = 0; f < NOUT; ++f) out[f * g.fs + c] = val[f];
+  for (int f = 0; f < NOUT; ++f) {
+#if FDNS_ST_CS
+    __stcs(out + f * g.fs + c, val[f]);
+#else
+    out[f * g.fs + c] = val[f];
+#endif
+  }
 }
 
 template <int NOUT>
@@ -401,20 +444,45 @@ struct Segments {
   int n0;             // planes per tile (SPLIT_ROUNDS: per unit) in this launch
   int64_t stride = 0; // SPLIT_ROUNDS: distance between this CTA's units (G * n0)
   int64_t tiles = 1;  // SPLIT_ROUNDS: column tiles per plane chunk
+  // SPLIT_ROUNDS: the whole rounds end at main_end; the units left over (fewer
+  // than G) are cut into G equal plane ranges [tbeg, tend) per CTA, so the
+  // last round keeps every SM busy instead of `left` of them
+  int64_t main_end = 0, tbeg = 0, tend = 0;
   __host__ __device__ __forceinline__ int64_t seg_end(int64_t x) const {
     const int64_t tile_end = (x / n0 + 1) * (int64_t)n0;
     return tile_end < end ? tile_end : end;
   }
+  // SPLIT_ROUNDS walk.  The kernels pass the three tail values from shared
+  // memory (tl = {main_end, tbeg, tend}, read only at segment changes):
+  // held in registers through the plane loop they pushed the 12-warp
+  // kernels over their 168-register budget (SN 14% slower with 52 B of
+  // spills).
+  // (32-bit arithmetic: a round-robin launch has < 2^31 steps, checked by
+  // the host launcher)
+  __host__ __device__ __forceinline__ int64_t seg_end_rr(int64_t x64, int64_t me, int64_t te) const {
+    const int x = (int)x64;
+    const int tile_end = (x / n0 + 1) * n0;
+    const int lim = x >= (int)me ? (int)te : (int)end;
+    return tile_end < lim ? tile_end : lim;
+  }
   // start of the segment after the one holding x (>= end: none)
-  __host__ __device__ __forceinline__ int64_t next(int64_t x) const {
-    return stride ? x - x % n0 + stride : seg_end(x);
+  __host__ __device__ __forceinline__ int64_t next_rr(int64_t x64, int64_t me64, int64_t tb64,
+                                                      int64_t te64) const {
+    const int x = (int)x64, me = (int)me64, tb = (int)tb64, te = (int)te64;
+    if (x < me) {
+      const int nx = x - x % n0 + (int)stride;
+      if (nx < me) return nx;
+      return tb < te ? tb64 : end;
+    }
+    const int e = (int)seg_end_rr(x64, me64, te64);
+    return e < te ? (int64_t)e : end;
   }
   // column tile and axis-0 plane (relative to the launch's first plane) of x
   __host__ __device__ __forceinline__ int64_t tile_of(int64_t x) const {
-    return stride ? (x / n0) % tiles : x / n0;
+    return stride ? (int64_t)(((int)x / n0) % (int)tiles) : x / n0;
   }
   __host__ __device__ __forceinline__ int plane_of(int64_t x) const {
-    return stride ? (int)((x / n0) / tiles * n0 + x % n0) : (int)(x % n0);
+    return stride ? ((int)x / n0) / (int)tiles * n0 + (int)x % n0 : (int)(x % n0);
   }
   // CTA b of G over `total` = tiles * planes steps.
   //  SPLIT_ALIGNED (needs G >= tiles): each tile gets floor or ceil of
@@ -441,7 +509,12 @@ struct Segments {
       // The caller sets `tiles` (column tiles per plane chunk).
       Segments r{b * (int64_t)planes, total, planes};
       r.stride = G * (int64_t)planes;
-      if (r.beg > total) r.beg = total;
+      const int64_t units = total / planes, rounds = units / G, left = units - rounds * G;
+      r.main_end = rounds * r.stride;
+      const int64_t tail = left * planes;   // steps of the last, partial round
+      r.tbeg = r.main_end + b * tail / G;
+      r.tend = r.main_end + (b + 1) * tail / G;
+      if (rounds == 0) r.beg = r.tbeg < r.tend ? r.tbeg : total;
       return r;
     }
     const int64_t tiles = total / planes;
@@ -475,6 +548,73 @@ struct Segments {
   }
 };
 
+// Lockstep of the round-robin split (RR): CTAs that stage neighbouring tiles
+// drift apart over the ~2500 steps of a 512^3 stage (there is no inter-CTA
+// sync), so the halo columns and rows their boxes share were fetched from
+// DRAM again by each of them (ncu at 512^3: SS stage kernel 36.5 GB of reads
+// for 23.6 GB of inputs).  Each CTA publishes the number of step barriers it
+// has passed; after a barrier one thread holds the CTA back while a
+// neighbour in the tile grid (CTA b +- 1, b +- ntk: the same round deals
+// them neighbouring tiles) is more than K steps behind.  The slowest CTA
+// never waits and the static split ends with it anyway, so the wait is
+// free; the halos now hit in L2 (SS 26.5 GB, 1.12x its inputs; stage kernel
+// 10.6 -> 9.8 ms).  Each CTA's slot is its own 128 B line: with the slots
+// packed, every publish invalidated the line its neighbours poll and a step
+// took twice as long.  The spin is bounded: a stale or foreign value can
+// only end the lockstep, never hang the GPU.
+constexpr int PROG_DONE = 0x7fffffff;
+constexpr int PROG_SLOTS = 1024;
+constexpr int PROG_STRIDE = 32;   // ints per slot
+constexpr int LS_TID = 5 * 32;    // the thread that publishes and waits
+__device__ int g_prog[PROG_SLOTS * PROG_STRIDE];
+__device__ __forceinline__ int ld_prog(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_prog(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// K = pf_saved bits 8..15 (0 = free running)
+__device__ __forceinline__ int ls_slack(int pf_saved) {
+  return gridDim.x <= PROG_SLOTS ? (pf_saved >> 8) & 0xff : 0;
+}
+__device__ __forceinline__ void ls_publish(int v) {
+  st_prog(&g_prog[blockIdx.x * PROG_STRIDE], v);
+}
+// progress of tile-grid neighbour j (0: b-1, 1: b+1, 2: b-ntk, 3: b+ntk)
+__device__ __forceinline__ int ls_neighbour(int j, int ntk) {
+  const int b = (int)blockIdx.x, G = (int)gridDim.x;
+  const int n = j == 0 ? b - 1 : (j == 1 ? b + 1 : (j == 2 ? b - ntk : b + ntk));
+  return n >= 0 && n < G ? ld_prog(&g_prog[n * PROG_STRIDE]) : PROG_DONE;
+}
+// after the barrier of step w: publish, then wait for the neighbours (v: their
+// progress as loaded before the barrier)
+__device__ __forceinline__ void ls_step(int& ls_k, int w, const int* v, int ntk) {
+  ls_publish(w + 1);
+  const int need = w + 1 - ls_k;
+  int m = min(min(v[0], v[1]), min(v[2], v[3]));
+  if (m >= need) return;
+  const long long t0 = clock64();
+  do {
+    m = min(min(ls_neighbour(0, ntk), ls_neighbour(1, ntk)),
+            min(ls_neighbour(2, ntk), ls_neighbour(3, ntk)));
+    if (clock64() - t0 > 400000LL) {   // ~200 us: leave the lockstep
+      ls_k = 0;
+      ls_publish(PROG_DONE);
+      return;
+    }
+  } while (m < need);
+}
+
+// the round-robin kernels' tail values {main_end, tbeg, tend} (see
+// Segments::next_rr); one instance per kernel instantiation that calls it
+template <int TAG>
+__device__ __forceinline__ volatile int64_t* tail_slot() {
+  __shared__ int64_t s[3];
+  return s;
+}
+
 #ifndef FDNS_EARLY_GV
 #define FDNS_EARLY_GV 1
 #endif
@@ -498,9 +638,18 @@ __global__ void __launch_bounds__(NT, 1)
   const int tk = tid % TK, tj = tid / TK;
   Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes, split, cuts);
   if constexpr (RR) S.tiles = (int64_t)ntk * ((g.n1 + TJ - 1) / TJ);
+  volatile int64_t* s_tail = nullptr;
+  if constexpr (RR) {
+    s_tail = tail_slot<V * 4 + MODE * 2 + (LAZY ? 1 : 0)>();
+    if (threadIdx.x == 0) { s_tail[0] = S.main_end; s_tail[1] = S.tbeg; s_tail[2] = S.tend; }
+  }
   // segment walk: contiguous tile-major ranges, or (RR) round-robin units
   auto seg_next = [&](int64_t x) -> int64_t {
-    if constexpr (RR) return S.next(x);
+    if constexpr (RR) return S.next_rr(x, s_tail[0], s_tail[1], s_tail[2]);
+    else return S.seg_end(x);
+  };
+  auto seg_end = [&](int64_t x) -> int64_t {
+    if constexpr (RR) return S.seg_end_rr(x, s_tail[0], s_tail[2]);
     else return S.seg_end(x);
   };
   auto tile_at = [&](int64_t x) -> int64_t {
@@ -511,7 +660,10 @@ __global__ void __launch_bounds__(NT, 1)
     if constexpr (RR) return S.plane_of(x);
     else return (int)(x % nplanes);
   };
-  if (S.beg >= S.end) return;
+  if (S.beg >= S.end) {
+    if (RR && ls_slack(pf_saved) && threadIdx.x == LS_TID) ls_publish(PROG_DONE);
+    return;
+  }
   trace(0);
 
   if (tid == 0) {
@@ -527,6 +679,11 @@ __global__ void __launch_bounds__(NT, 1)
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   trace(1);
+  // lockstep of the round-robin CTAs (after the wait: the previous stage's
+  // CTAs no longer publish)
+  int ls_k = 0;
+  if constexpr (RR) ls_k = ls_slack(pf_saved);
+  if (RR && ls_k && tid == LS_TID) ls_publish(0);
   const CUtensorMap* tmap = &tin;
   double* outp = out;
   const double coefp = coef;
@@ -556,7 +713,7 @@ __global__ void __launch_bounds__(NT, 1)
   int p_len = 0, p_c0 = 0, p_c1 = 0, p_plane = 0, p_slot = 0;
   auto enter_segment = [&]() {
     const int64_t tile = tile_at(p_seg);
-    p_len = (int)(S.seg_end(p_seg) - p_seg) + 4;
+    p_len = (int)(seg_end(p_seg) - p_seg) + 4;
     p_c0 = (int)(tile % ntk) * TK + g.h - 2;
     p_c1 = (int)(tile / ntk) * TJ + g.h - 2;
     p_plane = i_lo + plane_at(p_seg) - 2 + g.h;
@@ -583,7 +740,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
   };
   int stage_pos = 0;   // stream positions of one stage (steps + 4 per segment)
-  for (int64_t x = S.beg; x < S.end; x = seg_next(x)) stage_pos += (int)(S.seg_end(x) - x) + 4;
+  for (int64_t x = S.beg; x < S.end; x = seg_next(x)) stage_pos += (int)(seg_end(x) - x) + 4;
   int total_pos = stage_pos;   // issue limit: end of the current stage
   if (tid == 0)
     while (issued < total_pos && issued < NR) issue_next();
@@ -595,7 +752,7 @@ __global__ void __launch_bounds__(NT, 1)
     return x >= NR ? x - NR : x;
   };
   for (int64_t x = S.beg; x < S.end; x = seg_next(x)) {
-    const int64_t se = S.seg_end(x);
+    const int64_t se = seg_end(x);
     const int64_t tile = tile_at(x);
     const int k0 = (int)(tile % ntk) * TK, j0 = (int)(tile / ntk) * TJ;
     const int jj = j0 + tj, kk = k0 + tk;
@@ -603,6 +760,13 @@ __global__ void __launch_bounds__(NT, 1)
     const int toff = (tj + 2) * PK + (tk + 2);
     const int nsteps = (int)(se - x);
     const int i_seg = i_lo + plane_at(x);   // axis-0 index of step 0
+    if constexpr (RR) {
+      // the last round's plane ranges differ per CTA: free running from here
+      if (ls_k && x >= s_tail[0]) {
+        if (tid == LS_TID) ls_publish(PROG_DONE);
+        ls_k = 0;
+      }
+    }
     double q1[5], q2[5];   // SN axis-0 queues
     for (int t = 0; t < nsteps; ++t, ++w, ++gs, wsl = (wsl + 1 == NR ? 0 : wsl + 1)) {
       if (t == 0 && w > 0) {
@@ -626,6 +790,13 @@ __global__ void __launch_bounds__(NT, 1)
       if constexpr (MODE == 1) {
 #pragma unroll
         for (int f = 0; f < 5; ++f) sv[f] = saved[f * g.fs + cl];
+      }
+      int ls_v[4] = {PROG_DONE, PROG_DONE, PROG_DONE, PROG_DONE};
+      if constexpr (RR) {
+        if (ls_k && tid == LS_TID) {   // consumed after the step barrier
+#pragma unroll
+          for (int j = 0; j < 4; ++j) ls_v[j] = ls_neighbour(j, ntk);
+        }
       }
       double gv[9];
       if constexpr (kGB && FDNS_EARLY_GV) {
@@ -696,6 +867,9 @@ __global__ void __launch_bounds__(NT, 1)
       }
       __syncthreads();
       if (w == 0) trace(2);
+      if constexpr (RR) {
+        if (ls_k && tid == LS_TID) ls_step(ls_k, w, ls_v, ntk);
+      }
       if (tid == 0) {
         if (issued < total_pos && issued < w + NR) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -793,6 +967,7 @@ __global__ void __launch_bounds__(NT, 1)
     w += 4;   // the segment's trailing positions
     wsl = w % NR;
   }
+  if (RR && tid == LS_TID && ls_slack(pf_saved)) ls_publish(PROG_DONE);
   trace(3);
 }
 

@@ -264,9 +264,18 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
   const int tk = tid % TK, tj = tid / TK;
   Segments S = Segments::partition(blockIdx.x, gridDim.x, total_steps, nplanes, split, cuts);
   if constexpr (RR) S.tiles = (int64_t)ntk * ((g.n1 + TJ - 1) / TJ);
+  volatile int64_t* s_tail = nullptr;
+  if constexpr (RR) {
+    s_tail = tiled::tail_slot<64 + V * 2 + MODE>();
+    if (threadIdx.x == 0) { s_tail[0] = S.main_end; s_tail[1] = S.tbeg; s_tail[2] = S.tend; }
+  }
   // segment walk: contiguous tile-major ranges, or (RR) round-robin units
   auto seg_next = [&](int64_t x) -> int64_t {
-    if constexpr (RR) return S.next(x);
+    if constexpr (RR) return S.next_rr(x, s_tail[0], s_tail[1], s_tail[2]);
+    else return S.seg_end(x);
+  };
+  auto seg_end = [&](int64_t x) -> int64_t {
+    if constexpr (RR) return S.seg_end_rr(x, s_tail[0], s_tail[2]);
     else return S.seg_end(x);
   };
   auto tile_at = [&](int64_t x) -> int64_t {
@@ -277,7 +286,14 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
     if constexpr (RR) return S.plane_of(x);
     else return (int)(x % nplanes);
   };
-  if (S.beg >= S.end) return;
+  // lockstep (RR only): K = pf_saved bits 8..15, 0 = off
+  constexpr int LS_TID = tiled::LS_TID;   // the thread that publishes and waits
+  int ls_k = 0;
+  if constexpr (RR) ls_k = tiled::ls_slack(pf_saved);
+  if (S.beg >= S.end) {
+    if (RR && ls_k && tid == LS_TID) tiled::ls_publish(tiled::PROG_DONE);
+    return;
+  }
   tiled::trace(0);
 
   if (tid == 0) {
@@ -290,6 +306,8 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   tiled::trace(1);
+  // (after the wait: the previous stage's CTAs no longer publish)
+  if (RR && ls_k && tid == LS_TID) tiled::ls_publish(0);
 
   // SS/RS: the stored-gradient boxes of the centre plane of step gs
   auto issue_gb_tile = [&](int gs_, int k0, int j0, int plane) {
@@ -314,7 +332,7 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
   int p_len = 0, p_c0 = 0, p_c1 = 0, p_plane = 0, p_slot = 0;
   auto enter_segment = [&]() {
     const int64_t tile = tile_at(p_seg);
-    p_len = (int)(S.seg_end(p_seg) - p_seg) + 4;
+    p_len = (int)(seg_end(p_seg) - p_seg) + 4;
     p_c0 = (int)(tile % ntk) * TK + g.h - 2;
     p_c1 = (int)(tile / ntk) * TJ + g.h - 2;
     p_plane = i_lo + plane_at(p_seg) - 2 + g.h;
@@ -322,7 +340,11 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
   if (tid == 0) enter_segment();
   auto issue_next = [&]() {
     mbar_expect_tx(&bars[p_slot], LOAD_BYTES);
+#if FDNS_TMA_EL
+    tiled::tma_load_plane_el(sm + p_slot * SLOT, &tin, &bars[p_slot], p_c0, p_c1, p_plane + p_r);
+#else
     tma_load_plane(sm + p_slot * SLOT, &tin, &bars[p_slot], p_c0, p_c1, p_plane + p_r);
+#endif
     if (MODE == 1 && (pf_saved & tiled::PF_SAVED) && p_r >= 2 && p_r < p_len - 2)
       tma_prefetch_l2(&tsv, p_c0 + 2, p_c1 + 2, p_plane + p_r);
     // SS/RS: the nine stored gradients of this plane's tile columns into L2
@@ -337,7 +359,7 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
     }
   };
   int total_pos = 0;
-  for (int64_t x = S.beg; x < S.end; x = seg_next(x)) total_pos += (int)(S.seg_end(x) - x) + 4;
+  for (int64_t x = S.beg; x < S.end; x = seg_next(x)) total_pos += (int)(seg_end(x) - x) + 4;
   if (tid == 0)
     while (issued < total_pos && issued < NR) issue_next();
 
@@ -347,7 +369,7 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
     return x >= NR ? x - NR : x;
   };
   for (int64_t x = S.beg; x < S.end; x = seg_next(x)) {
-    const int64_t se = S.seg_end(x);
+    const int64_t se = seg_end(x);
     const int64_t tile = tile_at(x);
     const int k0 = (int)(tile % ntk) * TK, j0 = (int)(tile / ntk) * TJ;
     const int jj = j0 + tj, kk = k0 + tk;
@@ -356,6 +378,13 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
     const int hx = halo_pos<L>(tid < NT / 2 ? tid : tid - NT / 2);   // staggered halo item
     const int nsteps = (int)(se - x);
     const int i_seg = i_lo + plane_at(x);
+    if constexpr (RR) {
+      // the last round's plane ranges differ per CTA: free running from here
+      if (ls_k && x >= s_tail[0]) {
+        if (tid == LS_TID) tiled::ls_publish(tiled::PROG_DONE);
+        ls_k = 0;
+      }
+    }
     double q1[5], q2[5];
     for (int t = 0; t < nsteps; ++t, ++w, ++gs, wsl = (wsl + 1 == NR ? 0 : wsl + 1)) {
       if (t == 0 && w > 0) {
@@ -373,7 +402,7 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
       double sv[5];
       if constexpr (MODE == 1) {
 #pragma unroll
-        for (int f = 0; f < 5; ++f) sv[f] = saved[f * g.fs + cl];
+        for (int f = 0; f < 5; ++f) sv[f] = tiled::ld_stream(saved + f * g.fs + cl);
       }
       // SS/RS: the stored gradients this point FETCHes (plan.py:176-179):
       // the axis-0 queues of D(u1,x1), D(u2,x2) at this column and the six
@@ -397,12 +426,19 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
         }
       }
       if constexpr (kGB) {
-        gv[0 * 3 + 1] = __ldg(work + 1 * g.fs + cl);
-        gv[0 * 3 + 2] = __ldg(work + 2 * g.fs + cl);
-        gv[1 * 3 + 0] = __ldg(work + 3 * g.fs + cl);
-        gv[1 * 3 + 2] = __ldg(work + 5 * g.fs + cl);
-        gv[2 * 3 + 0] = __ldg(work + 6 * g.fs + cl);
-        gv[2 * 3 + 1] = __ldg(work + 7 * g.fs + cl);
+        gv[0 * 3 + 1] = tiled::ldg_stream(work + 1 * g.fs + cl);
+        gv[0 * 3 + 2] = tiled::ldg_stream(work + 2 * g.fs + cl);
+        gv[1 * 3 + 0] = tiled::ldg_stream(work + 3 * g.fs + cl);
+        gv[1 * 3 + 2] = tiled::ldg_stream(work + 5 * g.fs + cl);
+        gv[2 * 3 + 0] = tiled::ldg_stream(work + 6 * g.fs + cl);
+        gv[2 * 3 + 1] = tiled::ldg_stream(work + 7 * g.fs + cl);
+      }
+      int ls_v[4] = {tiled::PROG_DONE, tiled::PROG_DONE, tiled::PROG_DONE, tiled::PROG_DONE};
+      if constexpr (RR) {
+        if (ls_k && tid == LS_TID) {   // issued early: the latency runs under the conversion
+#pragma unroll
+          for (int j = 0; j < 4; ++j) ls_v[j] = tiled::ls_neighbour(j, ntk);
+        }
       }
       if constexpr (kStagger) {
         static_assert(4 * (PK + TJ) == NT / 2, "halo points = half the threads");
@@ -576,6 +612,9 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
       }
       __syncthreads();
       if (w == 0) tiled::trace(2);
+      if constexpr (RR) {
+        if (ls_k && tid == LS_TID) tiled::ls_step(ls_k, w, ls_v, ntk);
+      }
       if (tid == 0) {
         if (issued < total_pos && issued < w + NR + 1) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -620,6 +659,7 @@ __global__ void __launch_bounds__(Lay<TJ_>::NT, Lay<TJ_>::MINB)
     w += 4;
     wsl = w % NR;
   }
+  if (RR && tid == LS_TID && tiled::ls_slack(pf_saved)) tiled::ls_publish(tiled::PROG_DONE);
   tiled::trace(3);
 }
 

@@ -8,7 +8,8 @@ since-removed 12-warp SS/RS layout when the L2 prefetch of the stored
 gradients was on.  A race of that kind shows up here as
 run-to-run differences: the runs cover the 8-warp SS/RS/RA/SN kernel, the
 12-warp SN, RA, SS and RS kernels,
-the SS/RS round-robin split, forced small CTA counts
+the SS/RS/SN round-robin split (with its lockstep and its partial last
+round), forced small CTA counts
 (many segment transitions per CTA), ragged grids (partial tiles), and the
 gradient / saved-state prefetches both on and off.  compute-sanitizer is not
 available on the GPU pool; this is its stand-in.
@@ -43,6 +44,7 @@ def lib(built):
     lib.fdns_set_kernel_path(0)
     lib.fdns_set_tiled_grid(0)
     lib.fdns_set_rounds(-1)
+    lib.fdns_set_lockstep(-1)
     lib.fdns_set_prefetch(3)
 
 
@@ -66,7 +68,11 @@ CASES = [("SN", 2, (0, 5, 13), -1), ("SN", 5, (0, 5, 13), -1),
          ("SS", 5, (0, 5, 13), -1), ("SS", 5, (0,), 4),
          ("RS", 5, (0, 5, 13), -1), ("RS", 5, (0,), 4),
          ("SS", 0, (0, 5, 13), -1), ("SS", 0, (0,), 4),
-         ("RS", 0, (0, 5, 13), -1), ("RS", 0, (0,), 4)]
+         ("RS", 0, (0, 5, 13), -1), ("RS", 0, (0,), 4),
+         # round-robin units on a forced CTA count: whole rounds in lockstep,
+         # then the partial last round cut into per-CTA plane ranges
+         ("SS", 5, (5, 3), 4), ("SN", 5, (0, 5, 3), 4), ("RS", 5, (4,), 4),
+         ("SS", 0, (5, 3), 4), ("RS", 0, (4,), 4)]
 
 
 @pytest.mark.parametrize("variant,path,ctas_list,rounds", CASES)
