@@ -498,6 +498,40 @@ __global__ void __launch_bounds__(256, 4) k_fill_cross(double* __restrict__ wa, 
   }
 }
 
+// The same for two axis-2 neighbours per thread through 16-byte accesses
+// (k_grad_ss_pair's layout): 22 loads + 6 stores per pair instead of 48 + 12.
+__global__ void __launch_bounds__(256, 3) k_fill_cross_pair(double* __restrict__ wa, Coef k,
+                                                            Geom g) {
+  pdl_entry();
+  const int pk = (int)(blockIdx.x * 64 + 2 * threadIdx.x);   // padded column of the pair
+  const int kk = pk - g.h;
+  const int jj = blockIdx.y * blockDim.y + threadIdx.y;
+  const int ii = blockIdx.z;
+  if (kk < 0 || kk >= g.n2 || jj >= g.n1) return;
+  const int64_t c = (ii + g.h) * g.s0 + (jj + g.h) * g.s1 + pk;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const double* inner = wa + slot(j, S_U + j) * g.fs + c;
+    auto ld2 = [&](int64_t off) { return __ldg(reinterpret_cast<const double2*>(inner + off)); };
+#pragma unroll
+    for (int o = 0; o < 3; ++o) {
+      if (o == j) continue;
+      double2 d;
+      if (o < 2) {
+        const int64_t st = o == 0 ? g.s0 : g.s1;
+        const double2 p1 = ld2(st), m1 = ld2(-st), p2 = ld2(2 * st), m2 = ld2(-2 * st);
+        d.x = k.w1[o] * (p1.x - m1.x) + k.w2[o] * (p2.x - m2.x);
+        d.y = k.w1[o] * (p1.y - m1.y) + k.w2[o] * (p2.y - m2.y);
+      } else {
+        const double2 a = ld2(-2), b = ld2(0), e = ld2(2);
+        d.x = k.w1[2] * (b.y - a.y) + k.w2[2] * (e.x - a.x);
+        d.y = k.w1[2] * (e.x - b.x) + k.w2[2] * (e.y - a.y);
+      }
+      *reinterpret_cast<double2*>(wa + (S_DD + dd_index(j, o)) * g.fs + c) = d;
+    }
+  }
+}
+
 // SS/RS fill in one launch: the nine velocity gradients ws[q*3+a] =
 // D(u_q, x_a) on the interior, then the ghost frames of the three diagonal
 // ones (k_diag_ghost semantics).
@@ -1396,7 +1430,11 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
       launch_pdl(k_fill_bl_all<7>, grd, blk, 0, s, in, work, k, g);
     ghosts(work + slot(0, S_U + 0) * g.fs, work + slot(1, S_U + 1) * g.fs,
            work + slot(2, S_U + 2) * g.fs, true);
-    launch_pdl(k_fill_cross, grd, blk, 0, s, work, k, g);
+    if (g_ss_fill_pair && ss_pair_ok(g, in, work))
+      launch_pdl(k_fill_cross_pair, dim3((unsigned)((g.n2 + 2 * g.h + 63) / 64), grd.y, grd.z), blk,
+                 0, s, work, k, g);
+    else
+      launch_pdl(k_fill_cross, grd, blk, 0, s, work, k, g);
     count(3);
     return check_launch("BL fills");
   }
