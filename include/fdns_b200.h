@@ -161,6 +161,16 @@ void fdns_set_lockstep(int32_t slack);
  * [count, count x 5 words] to `out`. */
 int32_t fdns_debug_trace(int32_t enable, uint64_t* out, int32_t n);
 
+/* Host-side walk of the round-robin split (no GPU needed; a test hook for
+ * the partition the stage kernels use, fdns_tiled.cuh:Segments): `tiles`
+ * column tiles x `planes` planes in `unit`-plane units on `ctas` CTAs.
+ * cover[tile * planes + plane] is incremented once per visit (the caller
+ * zeroes it; every entry must end at 1), steps[b] receives CTA b's plane
+ * steps and segs[b] its segment count (either may be NULL).  Returns the
+ * number of CTAs launched (min(ctas, units)) or -1 on bad arguments. */
+int32_t fdns_debug_rounds_walk(int64_t tiles, int32_t planes, int32_t unit, int32_t ctas,
+                               int32_t* cover, int32_t* steps, int32_t* segs);
+
 /* Device reduction of the diagnostics of a state bundle (halos current):
  * out[0] = sum 0.5*rho*|u|^2, out[1] = sum 0.5*rho*|omega|^2, with rho from
  * `state` and the velocities (fields 5-7) from `prim_state` (NULL = state;

@@ -61,6 +61,8 @@ EXPORTS = {
     "fdns_set_rounds": (None, [_I]),
     "fdns_set_lockstep": (None, [_I]),
     "fdns_debug_trace": (_I, [_I, ctypes.POINTER(ctypes.c_uint64), _I]),
+    "fdns_debug_rounds_walk": (_I, [ctypes.c_int64, _I, _I, _I, ctypes.POINTER(_I),
+                                    ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "fdns_diag_partials_size": (_I, [ctypes.POINTER(Problem)]),
     "fdns_reduce_diag": (_I, [_VP, _VP, _VP, _VP, ctypes.POINTER(Problem),
                               _VP]),

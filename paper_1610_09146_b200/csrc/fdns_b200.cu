@@ -1504,6 +1504,31 @@ void fdns_set_prefetch(int32_t mask) {
   g_prefetch_grad = (mask & 2) != 0;
 }
 
+int32_t fdns_debug_rounds_walk(int64_t tiles, int32_t planes, int32_t unit, int32_t ctas,
+                               int32_t* cover, int32_t* steps, int32_t* segs) {
+  if (tiles <= 0 || planes <= 0 || unit <= 0 || planes % unit != 0 || ctas <= 0 || !cover)
+    return -1;
+  const int64_t total = tiles * planes;
+  if (total >= (1ll << 31)) return -1;
+  const int64_t G = std::min<int64_t>(ctas, total / unit);
+  for (int64_t b = 0; b < G; ++b) {
+    tiled::Segments S = tiled::Segments::partition(b, G, total, unit, tiled::SPLIT_ROUNDS);
+    S.tiles = tiles;
+    int32_t nst = 0, nsg = 0;
+    for (int64_t x = S.beg; x < S.end; x = S.next_rr(x, S.main_end, S.tbeg, S.tend)) {
+      const int64_t e = S.seg_end_rr(x, S.main_end, S.tend);
+      if (e <= x) return -1;   // a walk that does not advance
+      const int64_t tile = S.tile_of(x);
+      for (int64_t y = x; y < e; ++y) ++cover[tile * planes + S.plane_of(x) + (y - x)];
+      nst += (int32_t)(e - x);
+      ++nsg;
+    }
+    if (steps) steps[b] = nst;
+    if (segs) segs[b] = nsg;
+  }
+  return (int32_t)G;
+}
+
 int32_t fdns_debug_trace(int32_t enable, uint64_t* out, int32_t n) {
   int on = enable;
   if (cudaMemcpyToSymbol(tiled::g_trace_on, &on, sizeof(int)) != cudaSuccess)

@@ -50,3 +50,40 @@ def test_sm100a_code_in_library(built):
     out = subprocess.run([exe, "--list-elf", str(_lib.LIB_PATH)],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_round_robin_partition_covers_every_step_once(built):
+    """Host-side walk of the stage kernels' round-robin split
+    (fdns_tiled.cuh:Segments, SPLIT_ROUNDS with the partial last round cut
+    into per-CTA plane ranges): every (tile, plane) step is visited exactly
+    once and no CTA gets more than about its share -- no GPU needed."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_1610_09146_b200 import _lib
+    lib = _lib.load(require_gpu=False)
+    I32 = ctypes.POINTER(ctypes.c_int32)
+    # (tiles, planes, unit, ctas): the 512^3 launches (688 tiles of 32 x 12),
+    # 256^3 on the 8-warp kernel (8 x 32 tiles), tiny forced grids
+    cases = [(688, 512, 128, 148), (688, 512, 64, 148), (688, 512, 256, 148),
+             (256, 256, 128, 148), (176, 256, 64, 148), (2, 12, 4, 5),
+             (2, 16, 4, 3), (6, 24, 4, 4), (3, 8, 8, 148), (1, 4, 4, 148)]
+    for tiles, planes, unit, ctas in cases:
+        cover = np.zeros(tiles * planes, dtype=np.int32)
+        steps = np.zeros(ctas, dtype=np.int32)
+        segs = np.zeros(ctas, dtype=np.int32)
+        g = lib.fdns_debug_rounds_walk(tiles, planes, unit, ctas,
+                                       cover.ctypes.data_as(I32),
+                                       steps.ctypes.data_as(I32),
+                                       segs.ctypes.data_as(I32))
+        units = tiles * planes // unit
+        assert g == min(ctas, units), (tiles, planes, unit, ctas)
+        assert np.all(cover == 1), (tiles, planes, unit, ctas)
+        assert steps[:g].sum() == tiles * planes
+        # balance: whole rounds are equal, the tail differs by at most a step
+        assert steps[:g].max() - steps[:g].min() <= 1, (tiles, planes, unit, ctas)
+        # segments: the whole rounds plus at most two tail pieces
+        assert segs[:g].max() <= units // g + 2
+    bad = np.zeros(4, dtype=np.int32)
+    assert lib.fdns_debug_rounds_walk(1, 6, 4, 2, bad.ctypes.data_as(I32), None, None) == -1
