@@ -366,10 +366,32 @@ struct SQAcc {
   }
 };
 
+// Work-array stores of the fills: written once, read by a later kernel long
+// after they have left L2 -- evict-first (st.global.cs) keeps the 9 or 54
+// output streams from pushing the fills' own input planes (re-read by the
+// next planes' blocks) out of L2.  FDNS_FILL_CS=0: plain stores (A/B).
+#ifndef FDNS_FILL_CS
+#define FDNS_FILL_CS 1
+#endif
+__device__ __forceinline__ void st_fill(double* p, double v) {
+#if FDNS_FILL_CS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+__device__ __forceinline__ void st_fill2(double* p, double2 v) {
+#if FDNS_FILL_CS
+  __stcs(reinterpret_cast<double2*>(p), v);
+#else
+  *reinterpret_cast<double2*>(p) = v;
+#endif
+}
+
 template <int A_, int L>
 __device__ __forceinline__ void fill_axis_sq(const Coef& k, const SQAcc& a,
                                              double* __restrict__ wa, int64_t fs) {
-  wa[slot(A_, L) * fs + a.c] = eval_slot<A_, L>(k, a);
+  st_fill(&wa[slot(A_, L) * fs + a.c], eval_slot<A_, L>(k, a));
   if constexpr (L + 1 < S_PER_AXIS) fill_axis_sq<A_, L + 1>(k, a, wa, fs);
 }
 
@@ -527,7 +549,7 @@ __global__ void __launch_bounds__(256, 3) k_fill_cross_pair(double* __restrict__
         d.x = k.w1[2] * (b.y - a.y) + k.w2[2] * (e.x - a.x);
         d.y = k.w1[2] * (e.x - b.x) + k.w2[2] * (e.y - a.y);
       }
-      *reinterpret_cast<double2*>(wa + (S_DD + dd_index(j, o)) * g.fs + c) = d;
+      st_fill2(wa + (S_DD + dd_index(j, o)) * g.fs + c, d);
     }
   }
 }
@@ -659,9 +681,9 @@ __global__ void __launch_bounds__(256) k_grad_ss_pair(const double* __restrict__
     d2v.x = k.w1[2] * (b.y - a.y) + k.w2[2] * (e.x - a.x);
     d2v.y = k.w1[2] * (e.x - b.x) + k.w2[2] * (e.y - a.y);
     double* w = ws + (q * 3) * g.fs + c;
-    *reinterpret_cast<double2*>(w) = d[0];
-    *reinterpret_cast<double2*>(w + g.fs) = d[1];
-    *reinterpret_cast<double2*>(w + 2 * g.fs) = d2v;
+    st_fill2(w, d[0]);
+    st_fill2(w + g.fs, d[1]);
+    st_fill2(w + 2 * g.fs, d2v);
   }
 }
 // whether k_grad_ss_pair applies: 16-byte aligned pairs that never straddle
