@@ -380,13 +380,16 @@ __device__ __forceinline__ void st_fill(double* p, double v) {
   *p = v;
 #endif
 }
+template <bool CS>
 __device__ __forceinline__ void st_fill2(double* p, double2 v) {
-#if FDNS_FILL_CS
-  __stcs(reinterpret_cast<double2*>(p), v);
-#else
-  *reinterpret_cast<double2*>(p) = v;
-#endif
+  if constexpr (CS && FDNS_FILL_CS) __stcs(reinterpret_cast<double2*>(p), v);
+  else *reinterpret_cast<double2*>(p) = v;
 }
+// Measured whole RK3 steps (profiles/r02_fill_cs_ab.txt): at 512^3 SS +0.4%,
+// RS +0.5%, BL +1.5-2.5% (BL fill reads 18.5 -> 14.7 GB); at 256^3 and
+// 128^3 SS/RS lose 1.5% (the stage kernel then finds fewer of the freshly
+// written gradients in L2), so the paired kernels take it from 64M points.
+inline bool fill_cs(const Geom& g) { return (int64_t)g.n0 * g.n1 * g.n2 >= (64ll << 20); }
 
 template <int A_, int L>
 __device__ __forceinline__ void fill_axis_sq(const Coef& k, const SQAcc& a,
@@ -522,6 +525,7 @@ __global__ void __launch_bounds__(256, 4) k_fill_cross(double* __restrict__ wa, 
 
 // The same for two axis-2 neighbours per thread through 16-byte accesses
 // (k_grad_ss_pair's layout): 22 loads + 6 stores per pair instead of 48 + 12.
+template <bool CS>
 __global__ void __launch_bounds__(256, 3) k_fill_cross_pair(double* __restrict__ wa, Coef k,
                                                             Geom g) {
   pdl_entry();
@@ -549,7 +553,7 @@ __global__ void __launch_bounds__(256, 3) k_fill_cross_pair(double* __restrict__
         d.x = k.w1[2] * (b.y - a.y) + k.w2[2] * (e.x - a.x);
         d.y = k.w1[2] * (e.x - b.x) + k.w2[2] * (e.y - a.y);
       }
-      st_fill2(wa + (S_DD + dd_index(j, o)) * g.fs + c, d);
+      st_fill2<CS>(wa + (S_DD + dd_index(j, o)) * g.fs + c, d);
     }
   }
 }
@@ -643,6 +647,7 @@ __global__ void __launch_bounds__(256) k_grad_ss_interior(const double* __restri
 // arrays' ghost frames (k_diag_ghost semantics, f0 + f1 + f2 points; they
 // read only the state): dispatched last, they fill the launch's tail
 // instead of a separate, latency-bound 87 us kernel.
+template <bool CS>
 __global__ void __launch_bounds__(256) k_grad_ss_pair(const double* __restrict__ in,
                                                       double* __restrict__ ws, Coef k, Geom g,
                                                       int64_t f0, int64_t f1, int64_t f2) {
@@ -681,9 +686,9 @@ __global__ void __launch_bounds__(256) k_grad_ss_pair(const double* __restrict__
     d2v.x = k.w1[2] * (b.y - a.y) + k.w2[2] * (e.x - a.x);
     d2v.y = k.w1[2] * (e.x - b.x) + k.w2[2] * (e.y - a.y);
     double* w = ws + (q * 3) * g.fs + c;
-    st_fill2(w, d[0]);
-    st_fill2(w + g.fs, d[1]);
-    st_fill2(w + 2 * g.fs, d2v);
+    st_fill2<CS>(w, d[0]);
+    st_fill2<CS>(w + g.fs, d[1]);
+    st_fill2<CS>(w + 2 * g.fs, d2v);
   }
 }
 // whether k_grad_ss_pair applies: 16-byte aligned pairs that never straddle
@@ -1453,8 +1458,8 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
     ghosts(work + slot(0, S_U + 0) * g.fs, work + slot(1, S_U + 1) * g.fs,
            work + slot(2, S_U + 2) * g.fs, true);
     if (g_ss_fill_pair && ss_pair_ok(g, in, work))
-      launch_pdl(k_fill_cross_pair, dim3((unsigned)((g.n2 + 2 * g.h + 63) / 64), grd.y, grd.z), blk,
-                 0, s, work, k, g);
+      launch_pdl(fill_cs(g) ? k_fill_cross_pair<true> : k_fill_cross_pair<false>,
+                 dim3((unsigned)((g.n2 + 2 * g.h + 63) / 64), grd.y, grd.z), blk, 0, s, work, k, g);
     else
       launch_pdl(k_fill_cross, grd, blk, 0, s, work, k, g);
     count(3);
@@ -1473,7 +1478,8 @@ int launch_fills(int variant, const double* in, double* work, const Coef& k, con
       dim3 pgrd((unsigned)((g.n2 + 2 * g.h + 63) / 64), grd.y, grd.z);
       const int64_t per_layer = (int64_t)256 * pgrd.x * pgrd.y;
       pgrd.z += (unsigned)((f0 + f1 + f2 + per_layer - 1) / per_layer);
-      k_grad_ss_pair<<<pgrd, blk, 0, s>>>(in, work, k, g, f0, f1, f2);
+      if (fill_cs(g)) k_grad_ss_pair<true><<<pgrd, blk, 0, s>>>(in, work, k, g, f0, f1, f2);
+      else k_grad_ss_pair<false><<<pgrd, blk, 0, s>>>(in, work, k, g, f0, f1, f2);
       count(1);
     } else {
       k_grad_ss_interior<<<grd, blk, 0, s>>>(in, work, k, g);
