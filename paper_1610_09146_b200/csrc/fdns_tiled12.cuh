@@ -33,6 +33,15 @@
 // to stage the off-diagonal gradients, so its load/store unit is busier
 // than SN's (mio + lg throttle stalls ~0.8 vs ~0.4 cycles per instruction).
 //
+// Round-robin split in lockstep (end of round 2; SN from 512 planes, SS/RS
+// from 256): 128-plane units dealt round-robin, the CTAs held within two
+// step barriers of their tile-grid neighbours (tiled::ls_step) so the halo
+// columns and rows neighbouring boxes share hit in L2 (ncu at 512^3: SN
+// reads 25.5 -> 15.2 GB, SS 36.5 -> 26.7 GB per stage), and the partial
+// last round cut into per-CTA plane ranges; whole RK3 steps SN +2.6%, SS
+// +8.7%, RS +4.5% (profiles/r02_lockstep_ab.txt).  RA keeps the contiguous
+// split (-1 to -3% with the units).
+//
 // RA (round 2) runs on the same layout.  It taps the oldest plane off its
 // own column as well (the mixed terms re-expand D(u0,x0) at in-plane shifts
 // and D(u1,x1), D(u2,x2) on plane i-2), so its buffer set holds, instead of
