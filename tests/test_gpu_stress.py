@@ -103,3 +103,26 @@ def test_repeated_runs_bitwise_stable(lib, variant, path, ctas_list, rounds):
         lib.fdns_set_prefetch(3)
         lib.fdns_set_rounds(-1)
     assert runs >= 100
+
+
+@pytest.mark.parametrize("variant,path", [("SS", 5), ("SN", 5), ("RS", 0)])
+def test_lockstep_slack_does_not_change_results(lib, variant, path):
+    """The round-robin CTAs' lockstep (fdns_set_lockstep) only changes when
+    a CTA runs, never what it computes: free running (0), the tightest
+    slack (1), the default and a loose one are all bitwise the point
+    kernels' result, on a forced 5-CTA grid whose last round is partial."""
+    npts = (24, 24, 40)
+    cons = _cons(npts)
+    lib.fdns_set_kernel_path(1)
+    want = _run(npts, cons, variant, 2)
+    lib.fdns_set_kernel_path(path)
+    lib.fdns_set_rounds(4)
+    lib.fdns_set_tiled_grid(5)
+    try:
+        for slack in (0, 1, -1, 4):
+            lib.fdns_set_lockstep(slack)
+            for rep in range(3):
+                got = _run(npts, cons, variant, 2)
+                assert np.array_equal(got, want), (variant, slack, rep)
+    finally:
+        lib.fdns_set_lockstep(-1)
